@@ -1,0 +1,329 @@
+#!/usr/bin/env python
+"""Headline benchmark: PCG + TPMG V(1,1) solve of BASELINE.json config 3 (1024x1024x128,
+fp64) on the sm_100a path, one process per GPU.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One STEP = one complete PCG solve (x0 = 0 -> |r|/|r0| <= 1e-8) of the synthetic problem.
+N = 1: config 3.  N > 1 (torchrun): weak scaling, a (1024*px) x (1024*py) x 128 global grid,
+1024^2 x 128 columns per GPU, decomposed horizontally (columns never split).
+value = whole-job throughput in GDOF/s = global DOF x PCG iterations / second (max over
+ranks).  Extra keys give PCG iterations/s, V-cycle GDOF/s, the roofline of the dominant
+kernel (line-Jacobi sweep) and the CPU baseline (the oracle port on the host cores).
+--impl reference times the CPU restatement of the reference path (oracle/) on the host.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PCG+MG iterations/sec and GDOF/s per V-cycle; achieved HBM GB/s vs peak"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device, self.samples, self._stop = device, [], threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def proc_grid(n: int):
+    px = 1
+    while px * px < n:
+        px *= 2
+    px = min(px, n)
+    return px, n // px  # 1->(1,1) 2->(2,1) 4->(2,2) 8->(4,2)
+
+
+def make_problem(px: int, py: int):
+    from paper_1408_2981_b200 import synth
+
+    if px * py == 1:
+        return synth.baseline_config(3)
+    # config 4 (weak): 1024^2 x 128 per GPU, same h, operator and RHS distribution
+    return synth.make_problem(
+        1024 * px, 1024 * py, 128, omega2=1e-3, lambda2=1e-4, grading="quadratic", depth=8,
+        nu=1, tol=1e-8, h=1.0 / 1024, name=f"cfg4_weak_{px}x{py}")
+
+
+def cpu_port_sample(P, threads: int, iters: int = 2):
+    """Oracle port timed on the host cores: seconds per PCG iteration (from the solve's
+    ConvergenceHistory seconds column) on the same problem, `iters` iterations."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    from paper_1408_2981_b200 import synth
+
+    O.build()
+    o = O.OracleHierarchy.from_problem(P, threads=threads)
+    f = synth.x_fastest_to_k_fastest(P.rhs())
+    _, hist, it, st, secs = o.pcg(f, P.tol, iters, seconds=True)
+    per_iter = (secs[it] - secs[1]) / max(it - 1, 1) if it >= 2 else secs[it]
+    return per_iter, it
+
+
+def run_reference(args):
+    """--impl reference: the CPU restatement of the reference path (oracle port), all host
+    threads, bounded sample per step (2 PCG iterations of the same config)."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    P = make_problem(*proc_grid(world))
+    threads = os.cpu_count() or 1
+    per = []
+    for s in range(args.warmup + args.steps):
+        t, it = cpu_port_sample(P, threads, iters=2)
+        if s >= args.warmup:
+            per.append(t)
+    t_iter = statistics.median(per)
+    value = P.n_dof / t_iter / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GDOF/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_iter * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE configs)",
+        "config": {"workload": P.name, "nx": P.nx, "ny": P.ny, "nz": P.nz, "sample": "per step: 2 PCG iterations"},
+        "pcg_iterations_per_s": 1.0 / t_iter,
+        "cpu_baseline": {"value": value, "unit": "GDOF/s", "cores": threads, "kind": "port",
+                         "sample": f"{P.name}: PCG iterations 2.. of an oracle solve, per-iteration time"},
+        "e2e": {"value": value, "unit": "GDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--max-iter", type=int, default=500)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1408_2981_b200 import synth, tpmg
+
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo", init_method="env://")
+    px, py = proc_grid(world)
+    P = make_problem(px, py)
+    torch.cuda.set_device(local)
+
+    nccl_id = None
+    if world > 1:
+        obj = [tpmg.Context.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    ctx = tpmg.Context(device=local, rank=rank, world_size=world, px=px, py=py, nccl_id=nccl_id)
+    h = tpmg.Hierarchy(ctx, P)
+    lnx, lny, nz, x0, y0 = h.level_shape(h.finest)
+    f_host = synth.rhs_x_fastest(P.rhs_seed, P.nx, P.ny, P.nz, x0, y0, lnx, lny)
+    f = h.field().upload(f_host)
+    x = h.field()
+    stream = torch.cuda.ExternalStream(ctx.stream_handle(), device=local)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- warm-up ------------------------------------------------------------------------------
+    res = None
+    for _ in range(args.warmup):
+        res = tpmg.pcg_solve(h, f, x, P.tol, args.max_iter)
+    # ---- timed region: K solves, device time by CUDA events on the library stream -------------
+    launches0 = ctx.kernel_launches()
+    iters = []
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            res = tpmg.pcg_solve(h, f, x, P.tol, args.max_iter)
+            iters.append(res.iterations)
+        e1.record(stream)
+        e1.synchronize()
+    torch.cuda.synchronize()
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    launches = ctx.kernel_launches() - launches0
+    total_iters = sum(iters)
+    ms_per_step = ms / args.steps
+    it_per_s = total_iters / (ms / 1e3)
+    value = P.n_dof * it_per_s / 1e9
+
+    # ---- e2e: the same solve through the public API from pinned host memory ---------------------
+    n_local = lnx * lny * nz
+    f_pin = torch.from_numpy(f_host.reshape(-1)).pin_memory()
+    x_pin = torch.empty(n_local, dtype=torch.float64).pin_memory()
+    fnp, xnp = f_pin.numpy(), x_pin.numpy()
+    ef = h.field()
+    tpmg.pcg_solve(h, ef.upload(fnp), x, P.tol, args.max_iter)  # warm
+    barrier()
+    torch.cuda.synchronize()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_iters = 0
+    e2.record(stream)
+    for _ in range(args.steps):
+        ef.upload(fnp)
+        r2 = tpmg.pcg_solve(h, ef, x, P.tol, args.max_iter)
+        xnp[:] = x.download().reshape(-1)
+        e2e_iters += r2.iterations
+    e3.record(stream)
+    e3.synchronize()
+    barrier()
+    e2e_ms = max_over_ranks(e2.elapsed_time(e3))
+    e2e_value = P.n_dof * e2e_iters / (e2e_ms / 1e3) / 1e9
+
+    # ---- dominant kernel roofline (live CUDA-event timing on the library stream) -----------------
+    peak, peak_kind = _peaks()
+    C_cols, N_dof = lnx * lny, n_local
+    t_jac = h.time_kernel(tpmg.K_JACOBI, h.finest, reps=20)
+    jac_bytes = 24 * N_dof + 32 * C_cols  # read u, f; write u'; 4 per-column scalars
+    achieved = jac_bytes / (t_jac * 1e-3) / 1e9
+    kernels = {}
+    for name, kid, by in (("apply", tpmg.K_APPLY, 16 * N_dof + 32 * C_cols),
+                          ("jacobi_zero_guess", tpmg.K_JACOBI_ZERO, 16 * N_dof + 32 * C_cols),
+                          ("resid_restrict", tpmg.K_RESID_RESTRICT, 16 * N_dof + 2 * N_dof + 32 * C_cols),
+                          ("prolong_add", tpmg.K_PROLONG_ADD, 16 * N_dof + 2 * N_dof)):
+        t = h.time_kernel(kid, h.finest, reps=10)
+        kernels[name] = {"ms": t, "GBps": by / (t * 1e-3) / 1e9, "frac": by / (t * 1e-3) / 1e9 / peak}
+    # V-cycle alone
+    vz = h.field()
+    torch.cuda.synchronize()
+    e4, e5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e4.record(stream)
+    for _ in range(5):
+        vz.fill(0.0)
+        tpmg.v_cycle(h, f, vz)
+    e5.record(stream)
+    e5.synchronize()
+    vcycle_ms = e4.elapsed_time(e5) / 5
+
+    traffic = None
+    prof_json = os.path.join(ROOT, "profiles", "jacobi_traffic.json")
+    if os.path.exists(prof_json):
+        try:
+            with open(prof_json) as fh:
+                traffic = json.load(fh).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded counter-based RNG, BASELINE.json config shapes)",
+        "config": {"workload": P.name + (" (config 3)" if world == 1 else " (config 4 weak)"),
+                   "global_grid": [P.nx, P.ny, P.nz], "tile": [lnx, lny, nz],
+                   "solver": "PCG + TPMG V(1,1), line-Jacobi, linear/transpose transfers",
+                   "tol": P.tol, "levels": h.n_levels, "process_grid": [px, py],
+                   "l2": "inputs larger than L2 (1.07 GB per vector)"},
+        "pcg_iterations_per_s": it_per_s, "pcg_iterations_per_solve": iters,
+        "vcycle_gdof_per_s": N_dof / (vcycle_ms * 1e-3) / 1e9, "vcycle_ms": vcycle_ms,
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "kernel": "k_jacobi (line-Jacobi sweep, finest level)",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "algorithmic_bytes": jac_bytes, "launch_ms": t_jac,
+                     "peak_kind": peak_kind},
+        "kernels": kernels,
+        "e2e": {"value": e2e_value, "unit": "GDOF/s", "h2d_bytes_per_step": 8 * n_local,
+                "d2h_bytes_per_step": 8 * n_local, "ms_per_step": e2e_ms / args.steps},
+        "clocks": clk.summary(),
+    }
+    # ---- CPU baseline: oracle port on the host cores (rank 0, N = 1 only) -----------------------
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            threads = os.cpu_count() or 1
+            t_cpu, _ = cpu_port_sample(P, threads, iters=2)
+            line["cpu_baseline"] = {"value": P.n_dof / t_cpu / 1e9, "unit": "GDOF/s",
+                                    "cores": threads, "kind": "port",
+                                    "sample": f"{P.name}: PCG iteration 2 of an oracle solve "
+                                              f"({t_cpu:.2f} s/iteration)"}
+        except Exception as e:  # noqa: BLE001
+            line["cpu_baseline"] = {"value": None, "unit": "GDOF/s", "cores": 0, "kind": "port",
+                                    "sample": f"failed: {e}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,211 @@
+/*
+ * tpmg_b200.h -- C-ABI drop-in boundary of the B200-native tensor-product
+ * multigrid (TPMG) hot path: matrix-free operator apply, vertical line
+ * smoother, inter-grid transfers, V-cycle and the PCG driver, all fp64 and
+ * device resident on sm_100a.
+ *
+ * The reference (arXiv 1408.2981, `proj/include/tpmg/`) is a header-only C++20
+ * template library with no FFI of its own; every entry point below names the
+ * reference function it replaces (path:line relative to the reference root).
+ * Conventions carried over from the reference:
+ *   - levels are numbered like MultigridHierarchy (multigrid.hpp:207-235):
+ *     0 = coarsest ... n_levels-1 = finest;
+ *   - the reference's exception taxonomy (types.hpp:24-58) becomes the
+ *     tpmg_status return code, nothing is thrown across the ABI;
+ *   - fields are one scalar per (column, level); on the host the caller picks
+ *     the reference's k-fastest order (discretization.hpp:106-120, Field) or
+ *     the device's x-fastest order [k][y][x]; conversion is a permutation;
+ *   - horizontal grid: doubly periodic Cartesian nx*ny, cell (i,j) = j*nx+i,
+ *     neighbour order W,E,S,N (the Cartesian restatement of the icosahedral
+ *     neighbour tables, geometry.hpp:51-53); edge ids: east edge of cell c is
+ *     c, north edge of cell c is nx*ny + c.
+ * Ownership: handles are owned by the library; host buffers are only borrowed
+ * for the duration of a call.  All calls are stream ordered on the context's
+ * stream and synchronous at return.  A context is not shared across threads.
+ */
+#ifndef TPMG_B200_H
+#define TPMG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TPMG_ABI_VERSION 1
+
+typedef enum tpmg_status {
+  TPMG_OK = 0,
+  TPMG_E_CONFIG = 1,      /* config_error      types.hpp:24-28 */
+  TPMG_E_SHAPE = 2,       /* shape_error       types.hpp:30-34 */
+  TPMG_E_NONFINITE = 3,   /* nonfinite_error   types.hpp:36-40 */
+  TPMG_E_FINGERPRINT = 4, /* fingerprint_error types.hpp:42-46 */
+  TPMG_E_SINGULAR = 5,    /* singular_error    types.hpp:48-52 (zero Thomas pivot) */
+  TPMG_E_CAP = 6,         /* cap_error         types.hpp:54-58 */
+  TPMG_E_CUDA = 7,        /* CUDA runtime failure / extension missing */
+  TPMG_E_NCCL = 8,        /* NCCL failure */
+  TPMG_NOT_CONVERGED = 9, /* Krylov: max_iter reached */
+  TPMG_BREAKDOWN = 10,    /* Krylov: p.q <= 0 / rho == 0 */
+  TPMG_DIVERGED = 11      /* Krylov: |r|/|r0| > 1e4 */
+} tpmg_status;
+
+typedef enum tpmg_layout {
+  TPMG_LAYOUT_K_FASTEST = 0, /* reference Field order: (k, column), k fastest */
+  TPMG_LAYOUT_X_FASTEST = 1  /* device order [k][y][x] */
+} tpmg_layout;
+
+/* SmootherKind, relaxation.hpp:10. Only block_jacobi is data parallel; the
+ * device rejects block_sor with TPMG_E_CONFIG (sequential by contract,
+ * relaxation.hpp:13-16). */
+typedef enum tpmg_smoother_kind {
+  TPMG_SMOOTHER_BLOCK_JACOBI = 0,
+  TPMG_SMOOTHER_BLOCK_SOR = 1
+} tpmg_smoother_kind;
+
+/* ProlongationKind / RestrictionKind, multigrid.hpp:10-11. */
+typedef enum tpmg_prolongation_kind { TPMG_PROLONG_LINEAR = 0, TPMG_PROLONG_INJECTION = 1 } tpmg_prolongation_kind;
+typedef enum tpmg_restriction_kind { TPMG_RESTRICT_SUMMATION = 0, TPMG_RESTRICT_TRANSPOSE = 1 } tpmg_restriction_kind;
+
+typedef struct tpmg_context_s* tpmg_context;
+typedef struct tpmg_hierarchy_s* tpmg_hierarchy;
+typedef struct tpmg_field_s* tpmg_field;
+
+/* One context per GPU / rank.  world_size == 1 needs no NCCL id. */
+typedef struct tpmg_context_params {
+  int device;          /* CUDA ordinal; -1 = keep the current device */
+  int rank;            /* this process' rank */
+  int world_size;      /* number of ranks (GPUs) */
+  int px, py;          /* process grid, px*py == world_size; rank = ry*px + rx */
+  const void* nccl_id; /* 128-byte ncclUniqueId produced by rank 0, or NULL */
+} tpmg_context_params;
+
+/* Horizontal (Cartesian, doubly periodic) x vertical grid.
+ * VerticalGrid, geometry.hpp:98-111; flat analogue: faces z_0 < ... < z_nz,
+ * volumes dz_k = z_{k+1} - z_k, Neumann masks on both boundary faces. */
+typedef struct tpmg_grid_desc {
+  int64_t nx, ny;        /* GLOBAL cell counts */
+  double hx, hy;         /* cell widths (areas hx*hy; edge factors hy/hx, hx/hy) */
+  int64_t nz;            /* vertical cells */
+  const double* z_faces; /* nz+1 strictly increasing face heights */
+} tpmg_grid_desc;
+
+/* FactorizedProfileSet, profiles.hpp:196-210: four vertical vectors and four
+ * horizontal scalar fields.  Horizontal arrays are GLOBAL (nx*ny / 2*nx*ny);
+ * each rank extracts its tile. */
+typedef struct tpmg_factorized_profiles {
+  const double* beta_r;    /* nz   */
+  const double* alpha_s_r; /* nz   */
+  const double* alpha_r_r; /* nz+1 */
+  const double* xi_r_r;    /* nz+1, NULL = no vertical advection */
+  const double* beta_s;    /* nx*ny   */
+  const double* alpha_r_s; /* nx*ny   */
+  const double* xi_r_s;    /* nx*ny, NULL = no vertical advection */
+  const double* alpha_s_s; /* 2*nx*ny: east edges, then north edges */
+} tpmg_factorized_profiles;
+
+/* Arguments of build_hierarchy_coefficients, multigrid.hpp:242-272. */
+typedef struct tpmg_mg_config {
+  int smoother;     /* tpmg_smoother_kind */
+  double relax;     /* SmootherConfig::relax, must lie in (0,2) (relaxation.hpp:67-68) */
+  int prolongation; /* tpmg_prolongation_kind */
+  int restriction;  /* tpmg_restriction_kind */
+  int nu_pre;       /* sweeps on refined levels; coarsest is forced to 1+0 (multigrid.hpp:269-270) */
+  int nu_post;
+  int depth;        /* number of levels; 0 = coarsen while every tile dim stays even and >= 2 */
+} tpmg_mg_config;
+
+/* ---- context ------------------------------------------------------------------------------ */
+const char* tpmg_status_string(int status);
+int tpmg_abi_version(void);
+/* Fills 128 bytes with a fresh ncclUniqueId (rank 0 calls this, then broadcasts). */
+int tpmg_nccl_unique_id(void* out128);
+int tpmg_init(const tpmg_context_params* params, tpmg_context* out);
+int tpmg_finalize(tpmg_context ctx);
+const char* tpmg_last_error(tpmg_context ctx);
+/* The cudaStream_t every call of this context is ordered on (for external CUDA-event timing). */
+int tpmg_context_stream(tpmg_context ctx, void** stream);
+
+/* ---- hierarchy: build_hierarchy_coefficients (multigrid.hpp:242-272) ---------------------- */
+/* assemble_hatted (discretization.hpp:144-184) on every level after
+ * restrict_profiles (multigrid.hpp:158-201); uploads the result, immutable. */
+int tpmg_hier_create(tpmg_context ctx, const tpmg_grid_desc* grid,
+                     const tpmg_factorized_profiles* profiles, double omega,
+                     const tpmg_mg_config* cfg, tpmg_hierarchy* out);
+int tpmg_hier_destroy(tpmg_hierarchy h);
+int tpmg_hier_n_levels(tpmg_hierarchy h, int* n_levels);
+/* Local tile shape and global offset of `level` on this rank. */
+int tpmg_hier_level_shape(tpmg_hierarchy h, int level, int64_t* nx, int64_t* ny, int64_t* nz,
+                          int64_t* x0, int64_t* y0);
+/* Hatted coefficients of `level` (HattedCoefficients, discretization.hpp:53-67), tile local:
+ * bh/ah/xh: nx*ny; sh: 2*nx*ny (east, north); bv/sv: nz; av/xv: nz+1.  Any pointer may be NULL. */
+int tpmg_hier_get_coefficients(tpmg_hierarchy h, int level, double* bh, double* ah, double* xh,
+                               double* sh, double* bv, double* sv, double* av, double* xv);
+
+/* ---- fields: Field (discretization.hpp:106-120), device resident [k][y][x] ---------------- */
+int tpmg_field_create(tpmg_hierarchy h, int level, tpmg_field* out);
+int tpmg_field_destroy(tpmg_field f);
+int tpmg_field_level(tpmg_field f, int* level);
+int tpmg_field_upload(tpmg_field f, const double* host, int layout);
+int tpmg_field_download(tpmg_field f, double* host, int layout);
+int tpmg_field_fill(tpmg_field f, double value);
+int tpmg_field_copy(tpmg_field dst, tpmg_field src);
+/* Raw device pointer ([k][y][x], nx*ny*nz doubles) for zero-copy interop. */
+int tpmg_field_device_ptr(tpmg_field f, double** out);
+
+/* ---- hot path ------------------------------------------------------------------------------ */
+/* apply_operator, discretization.hpp:262-278: y = A u on u's level. */
+int tpmg_apply(tpmg_hierarchy h, tpmg_field u, tpmg_field y);
+/* r = f - A u (multigrid.hpp:285-287). */
+int tpmg_residual(tpmg_hierarchy h, tpmg_field f, tpmg_field u, tpmg_field r);
+/* smooth, relaxation.hpp:63-97 (block_jacobi): `sweeps` line-Jacobi sweeps on u. */
+int tpmg_smooth(tpmg_hierarchy h, tpmg_field u, tpmg_field f, int sweeps);
+/* restrict_field / restrict_field_transpose, multigrid.hpp:29-69 (kind from the config). */
+int tpmg_restrict(tpmg_hierarchy h, tpmg_field fine, tpmg_field coarse);
+/* prolongate_field + `u +=`, multigrid.hpp:74-100, :294-295 (kind from the config). */
+int tpmg_prolong_add(tpmg_hierarchy h, tpmg_field coarse, tpmg_field fine);
+/* prolongate_field alone: fine = P coarse. */
+int tpmg_prolong(tpmg_hierarchy h, tpmg_field coarse, tpmg_field fine);
+/* v_cycle(m, finest, f, u), multigrid.hpp:276-299: one V-cycle, u updated in place. */
+int tpmg_vcycle(tpmg_hierarchy h, tpmg_field f, tpmg_field u);
+/* measure_cycle_rate, multigrid.hpp:302-321. */
+int tpmg_measure_cycle_rate(tpmg_hierarchy h, tpmg_field f, int n_cycles, double* rate);
+/* Global (all-reduced) dot product and Euclidean norm (Field::norm, discretization.hpp:27). */
+int tpmg_dot(tpmg_hierarchy h, tpmg_field a, tpmg_field b, double* out);
+int tpmg_norm(tpmg_hierarchy h, tpmg_field a, double* out);
+
+/* PCG preconditioned by one V-cycle from a zero guess (SPEC.md:387-448 conventions):
+ * x0 = 0 (x is overwritten), stop when |r_k|/|r_0| <= tol, divergence at > 1e4.
+ * res_hist (may be NULL) receives |r_0| .. |r_iters| (max_iter+1 entries);
+ * solve_status receives TPMG_OK / NOT_CONVERGED / BREAKDOWN / DIVERGED.
+ * The return value is TPMG_OK unless the call itself failed. */
+int tpmg_pcg(tpmg_hierarchy h, tpmg_field f, tpmg_field x, double tol, int max_iter,
+             double* res_hist, int* iters, int* solve_status);
+
+/* End-to-end solve from host memory: upload f (layout), PCG, download x. */
+int tpmg_pcg_host(tpmg_hierarchy h, const double* f_host, double* x_host, int layout, double tol,
+                  int max_iter, double* res_hist, int* iters, int* solve_status);
+
+/* ---- instrumentation ------------------------------------------------------------------------ */
+/* Number of kernels this library launched on the context since creation. */
+int tpmg_kernel_launch_count(tpmg_context ctx, int64_t* out);
+/* Kernel ids for tpmg_time_kernel. */
+typedef enum tpmg_kernel_id {
+  TPMG_K_APPLY = 0,           /* y = A u                                  */
+  TPMG_K_JACOBI = 1,          /* one line-Jacobi sweep, nonzero guess     */
+  TPMG_K_JACOBI_ZERO = 2,     /* one line-Jacobi sweep from a zero guess  */
+  TPMG_K_RESID_RESTRICT = 3,  /* coarse = R (f - A u) as used by the V-cycle */
+  TPMG_K_PROLONG_ADD = 4,     /* fine += P coarse                         */
+  TPMG_K_RESTRICT = 5,        /* coarse = R fine                          */
+  TPMG_K_RESIDUAL = 6         /* r = f - A u                              */
+} tpmg_kernel_id;
+/* Average device time (CUDA events on the library's stream) of `reps` back-to-back launches
+ * of one hot-path kernel on `level` (transfers: `level` is the fine level), on internal
+ * scratch fields filled with deterministic data.  Instrumentation for bench.py. */
+int tpmg_time_kernel(tpmg_hierarchy h, int kernel_id, int level, int reps, double* avg_ms);
+/* Enable/disable CUDA-graph replay of the PCG iteration (default on). */
+int tpmg_set_use_graphs(tpmg_hierarchy h, int enable);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TPMG_B200_H */

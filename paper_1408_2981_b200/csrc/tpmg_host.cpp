@@ -1,0 +1,1076 @@
+// tpmg_host.cpp -- C-ABI implementation (include/tpmg_b200.h): hierarchy setup, device
+// resident fields, the V-cycle / PCG drivers and the NCCL halo + all-reduce plumbing.
+//
+// Setup restates the reference's hierarchy construction for the doubly periodic Cartesian
+// grid (assemble_hatted, discretization.hpp:144-184; restrict_profiles, multigrid.hpp:158-201;
+// build_hierarchy_coefficients, multigrid.hpp:242-272) on the host, once; every hot-path
+// operation runs as sm_100a kernels (tpmg_kernels.cu) on the context's stream.  There is
+// no CPU fallback: without a CUDA device every entry point returns TPMG_E_CUDA.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/tpmg_b200.h"
+#include "tpmg_kernels.cuh"
+
+namespace {
+
+using tpmg::Halo;
+using tpmg::LevelCoef;
+using tpmg::VertCoef;
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& w) : std::runtime_error(w), code(c) {}
+};
+
+#define CUDA_CHECK(x)                                                                   \
+  do {                                                                                  \
+    cudaError_t e_ = (x);                                                               \
+    if (e_ != cudaSuccess)                                                              \
+      throw Error(TPMG_E_CUDA, std::string(#x ": ") + cudaGetErrorString(e_));          \
+  } while (0)
+
+// ---- NCCL, resolved lazily (single-GPU runs never load it) ------------------------------
+struct Nccl {
+  void* handle = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+
+  void load() {
+    if (handle) return;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names)
+      if ((handle = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
+    if (!handle) throw Error(TPMG_E_NCCL, "cannot load libnccl.so.2");
+    auto sym = [&](const char* s) {
+      void* p = dlsym(handle, s);
+      if (!p) throw Error(TPMG_E_NCCL, std::string("NCCL symbol missing: ") + s);
+      return p;
+    };
+    GetUniqueId = (decltype(GetUniqueId))sym("ncclGetUniqueId");
+    CommInitRank = (decltype(CommInitRank))sym("ncclCommInitRank");
+    CommDestroy = (decltype(CommDestroy))sym("ncclCommDestroy");
+    Send = (decltype(Send))sym("ncclSend");
+    Recv = (decltype(Recv))sym("ncclRecv");
+    GroupStart = (decltype(GroupStart))sym("ncclGroupStart");
+    GroupEnd = (decltype(GroupEnd))sym("ncclGroupEnd");
+    AllReduce = (decltype(AllReduce))sym("ncclAllReduce");
+    GetErrorString = (decltype(GetErrorString))sym("ncclGetErrorString");
+  }
+};
+Nccl g_nccl;
+
+#define NCCL_CHECK(x)                                                                   \
+  do {                                                                                  \
+    ncclResult_t r_ = (x);                                                              \
+    if (r_ != ncclSuccess)                                                              \
+      throw Error(TPMG_E_NCCL, std::string(#x ": ") + g_nccl.GetErrorString(r_));       \
+  } while (0)
+
+thread_local std::string g_global_error;
+
+}  // namespace
+
+// ---- handles ------------------------------------------------------------------------------
+struct tpmg_context_s {
+  int device = 0;
+  int rank = 0, world = 1, px = 1, py = 1, rx = 0, ry = 0;
+  cudaStream_t stream = nullptr;
+  ncclComm_t comm = nullptr;
+  std::string last_error;
+  int64_t launches = 0;
+  tpmg::Launch launch() { return tpmg::Launch{stream, &launches}; }
+  int rank_of(int x, int y) const {
+    x = (x % px + px) % px;
+    y = (y % py + py) % py;
+    return y * px + x;
+  }
+};
+
+namespace {
+
+struct DevBuf {
+  double* p = nullptr;
+  size_t n = 0;
+  void alloc(size_t count) {
+    n = count;
+    CUDA_CHECK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(double)));
+  }
+  void upload(const double* h, size_t count) {
+    alloc(count);
+    CUDA_CHECK(cudaMemcpy(p, h, count * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+struct Level {
+  int nx = 0, ny = 0;          // local tile
+  int gnx = 0, gny = 0;        // global level dims
+  int x0 = 0, y0 = 0;          // tile offset (global cell index)
+  int64_t plane = 0;
+  // host copies of the hatted horizontal factors (tile local)
+  std::vector<double> bh, ah, xh, sh;  // sh: 2*plane (east, north)
+  DevBuf d_bh, d_ah, d_xh, d_sw, d_se, d_ss, d_sn;
+  DevBuf u, t, f;              // V-cycle work: home iterate, ping-pong partner, rhs
+  DevBuf send, recv;           // multi-GPU face buffers [W|E|S|N]
+  LevelCoef coef(int nz) const {
+    LevelCoef c;
+    c.nx = nx; c.ny = ny; c.nz = nz; c.plane = plane;
+    c.bh = d_bh.p; c.ah = d_ah.p; c.xh = d_xh.p;
+    c.sw = d_sw.p; c.se = d_se.p; c.ss = d_ss.p; c.sn = d_sn.p;
+    return c;
+  }
+};
+
+}  // namespace
+
+struct tpmg_hierarchy_s {
+  tpmg_context ctx = nullptr;
+  int nz = 0;
+  bool xi = false;
+  double relax = 1.0;
+  int prolongation = 0, restriction = 0;
+  std::vector<int> nu_pre, nu_post;
+  std::vector<Level> lv;  // coarsest .. finest
+  std::vector<double> bv, sv, av, xv;
+  DevBuf d_bv, d_sv, d_av, d_xv;
+  // finest-level PCG / V-cycle work vectors
+  DevBuf r, z, p, q, tmp;
+  DevBuf partials, scal;  // reduction partials; scalars s[0..7]
+  int* d_err = nullptr;
+  double* h_scal = nullptr;  // pinned
+  bool use_graphs = true;
+  std::unordered_map<const double*, cudaGraphExec_t> iter_graphs;
+  std::unordered_map<const double*, int64_t> iter_graph_kernels;
+  int finest() const { return (int)lv.size() - 1; }
+  VertCoef vcoef() const { return VertCoef{d_bv.p, d_sv.p, d_av.p, d_xv.p}; }
+  ~tpmg_hierarchy_s() {
+    for (auto& kv : iter_graphs) cudaGraphExecDestroy(kv.second);
+    if (d_err) cudaFree(d_err);
+    if (h_scal) cudaFreeHost(h_scal);
+  }
+};
+
+struct tpmg_field_s {
+  tpmg_hierarchy h = nullptr;
+  int level = 0;
+  DevBuf buf;
+};
+
+namespace {
+
+template <typename Fn>
+int guard(tpmg_context ctx, Fn&& fn) {
+  try {
+    fn();
+    return TPMG_OK;
+  } catch (const Error& e) {
+    if (ctx) ctx->last_error = e.what();
+    g_global_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    if (ctx) ctx->last_error = "host allocation failed";
+    return TPMG_E_CUDA;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->last_error = e.what();
+    g_global_error = e.what();
+    return TPMG_E_CONFIG;
+  }
+}
+
+void check_finite(const double* p, size_t n, const char* what) {
+  if (!p) throw Error(TPMG_E_CONFIG, std::string("missing array ") + what);
+  for (size_t i = 0; i < n; ++i)
+    if (!std::isfinite(p[i]))
+      throw Error(TPMG_E_NONFINITE, std::string("non-finite values in ") + what);
+}
+
+// ---- halos -----------------------------------------------------------------------------
+// Exchange the 1-cell faces of u on level l with the 4 neighbouring ranks and return the
+// view the kernels read across the tile faces.  Dimensions with a single rank wrap onto the
+// tile itself (periodic) without any copy.
+Halo exchange(tpmg_hierarchy h, int l, const double* u) {
+  tpmg_context ctx = h->ctx;
+  Level& L = h->lv[l];
+  Halo H = tpmg::self_halo(u, L.nx, L.ny, L.plane);
+  if (ctx->world == 1) return H;
+  const int nz = h->nz;
+  const int64_t nwe = (int64_t)L.ny * nz, nsn = (int64_t)L.nx * nz;
+  tpmg::launch_pack_faces(ctx->launch(), L.nx, L.ny, nz, u, L.send.p);
+  double* sW = L.send.p;
+  double* sE = sW + nwe;
+  double* sS = sE + nwe;
+  double* sN = sS + nsn;
+  double* rW = L.recv.p;
+  double* rE = rW + nwe;
+  double* rS = rE + nwe;
+  double* rN = rS + nsn;
+  NCCL_CHECK(g_nccl.GroupStart());
+  if (ctx->px > 1) {
+    const int west = ctx->rank_of(ctx->rx - 1, ctx->ry), east = ctx->rank_of(ctx->rx + 1, ctx->ry);
+    NCCL_CHECK(g_nccl.Send(sW, nwe, ncclDouble, west, ctx->comm, ctx->stream));
+    NCCL_CHECK(g_nccl.Send(sE, nwe, ncclDouble, east, ctx->comm, ctx->stream));
+    NCCL_CHECK(g_nccl.Recv(rE, nwe, ncclDouble, east, ctx->comm, ctx->stream));
+    NCCL_CHECK(g_nccl.Recv(rW, nwe, ncclDouble, west, ctx->comm, ctx->stream));
+  }
+  if (ctx->py > 1) {
+    const int south = ctx->rank_of(ctx->rx, ctx->ry - 1), north = ctx->rank_of(ctx->rx, ctx->ry + 1);
+    NCCL_CHECK(g_nccl.Send(sS, nsn, ncclDouble, south, ctx->comm, ctx->stream));
+    NCCL_CHECK(g_nccl.Send(sN, nsn, ncclDouble, north, ctx->comm, ctx->stream));
+    NCCL_CHECK(g_nccl.Recv(rN, nsn, ncclDouble, north, ctx->comm, ctx->stream));
+    NCCL_CHECK(g_nccl.Recv(rS, nsn, ncclDouble, south, ctx->comm, ctx->stream));
+  }
+  NCCL_CHECK(g_nccl.GroupEnd());
+  if (ctx->px > 1) {
+    H.p[0] = rW; H.sk[0] = L.ny; H.st[0] = 1;
+    H.p[1] = rE; H.sk[1] = L.ny; H.st[1] = 1;
+  }
+  if (ctx->py > 1) {
+    H.p[2] = rS; H.sk[2] = L.nx; H.st[2] = 1;
+    H.p[3] = rN; H.sk[3] = L.nx; H.st[3] = 1;
+  }
+  return H;
+}
+
+// s[slot] = global sum of the per-block partials.
+void finish_dot(tpmg_hierarchy h, int nblocks, int slot) {
+  tpmg_context ctx = h->ctx;
+  tpmg::launch_reduce(ctx->launch(), h->partials.p, nblocks, h->scal.p + slot);
+  if (ctx->world > 1)
+    NCCL_CHECK(g_nccl.AllReduce(h->scal.p + slot, h->scal.p + slot, 1, ncclDouble, ncclSum,
+                                ctx->comm, ctx->stream));
+}
+
+void dot_into(tpmg_hierarchy h, int64_t n, const double* a, const double* b, int slot) {
+  int nb = 0;
+  tpmg::launch_dot(h->ctx->launch(), n, a, b, h->partials.p, &nb);
+  finish_dot(h, nb, slot);
+}
+
+// ---- hot-path building blocks ------------------------------------------------------------
+void apply_level(tpmg_hierarchy h, int l, int mode, const double* u, const double* f, double* y,
+                 int dot_slot = -1) {
+  Level& L = h->lv[l];
+  const Halo H = exchange(h, l, u);
+  int nb = 0;
+  tpmg::launch_apply(h->ctx->launch(), h->vcoef(), L.coef(h->nz), h->xi, mode, u, H, f, y,
+                     dot_slot >= 0 ? h->partials.p : nullptr, &nb);
+  if (dot_slot >= 0) finish_dot(h, nb, dot_slot);
+}
+
+void sweep(tpmg_hierarchy h, int l, const double* u_in, const double* f, double* out) {
+  Level& L = h->lv[l];
+  Halo H = u_in ? exchange(h, l, u_in) : tpmg::self_halo(out, L.nx, L.ny, L.plane);
+  tpmg::launch_jacobi(h->ctx->launch(), h->vcoef(), L.coef(h->nz), h->xi, u_in, H, f, out,
+                      h->relax, h->d_err);
+}
+
+// fine level lf -> coarse lf-1: coarse = R (f - A u).  `scratch` is a free fine-level buffer.
+void resid_restrict(tpmg_hierarchy h, int lf, const double* u, const double* f, double* coarse,
+                    double* scratch) {
+  Level& F = h->lv[lf];
+  Level& C = h->lv[lf - 1];
+  if (h->restriction == TPMG_RESTRICT_SUMMATION) {
+    const Halo H = exchange(h, lf, u);
+    tpmg::launch_resid_restrict_sum(h->ctx->launch(), h->vcoef(), F.coef(h->nz), h->xi, u, H, f,
+                                    coarse);
+  } else {
+    apply_level(h, lf, tpmg::APPLY_RESID, u, f, scratch);
+    const Halo Hr = exchange(h, lf, scratch);
+    tpmg::launch_restrict_transpose(h->ctx->launch(), C.nx, C.ny, h->nz, scratch, Hr, coarse);
+  }
+}
+
+void restrict_plain(tpmg_hierarchy h, int lf, const double* fine, double* coarse) {
+  Level& C = h->lv[lf - 1];
+  if (h->restriction == TPMG_RESTRICT_SUMMATION) {
+    tpmg::launch_restrict_sum(h->ctx->launch(), C.nx, C.ny, h->nz, fine, coarse);
+  } else {
+    const Halo Hf = exchange(h, lf, fine);
+    tpmg::launch_restrict_transpose(h->ctx->launch(), C.nx, C.ny, h->nz, fine, Hf, coarse);
+  }
+}
+
+void prolong_level(tpmg_hierarchy h, int lc, const double* coarse, double* fine, bool add) {
+  Level& F = h->lv[lc + 1];
+  const bool linear = h->prolongation == TPMG_PROLONG_LINEAR;
+  const Halo Hc = linear ? exchange(h, lc, coarse) : Halo{};
+  tpmg::launch_prolong(h->ctx->launch(), F.nx, F.ny, h->nz, coarse, Hc, fine, linear, add);
+}
+
+void fill(tpmg_hierarchy h, double* p, int64_t n, double v) {
+  if (v == 0.0) CUDA_CHECK(cudaMemsetAsync(p, 0, n * sizeof(double), h->ctx->stream));
+  else tpmg::launch_fill(h->ctx->launch(), n, p, v);
+}
+
+// v_cycle, multigrid.hpp:276-299.  On return the iterate is in A; B is scratch of the same
+// level.  zero: A's content is ignored and treated as 0 (the preconditioner / coarse case).
+void vcycle(tpmg_hierarchy h, int l, const double* f, double* A, double* B, bool zero) {
+  Level& L = h->lv[l];
+  const int64_t n = L.plane * h->nz;
+  const int npre = h->nu_pre[l], npost = h->nu_post[l], total = npre + npost;
+  double* cur = A;
+  auto other = [&](double* c) { return c == A ? B : A; };
+  int s0 = 0;
+  if (zero) {
+    if (npre > 0) {
+      // first sweep from zero writes where the last sweep must end in A
+      cur = ((total - 1) % 2 == 0) ? A : B;
+      sweep(h, l, nullptr, f, cur);
+      s0 = 1;
+    } else {
+      cur = (npost % 2 == 0) ? A : B;
+      fill(h, cur, n, 0.0);
+    }
+  }
+  for (int s = s0; s < npre; ++s) {
+    double* out = other(cur);
+    sweep(h, l, cur, f, out);
+    cur = out;
+  }
+  if (l > 0) {
+    Level& C = h->lv[l - 1];
+    resid_restrict(h, l, cur, f, C.f.p, other(cur));
+    vcycle(h, l - 1, C.f.p, C.u.p, C.t.p, true);
+    prolong_level(h, l - 1, C.u.p, cur, true);
+  }
+  for (int s = 0; s < npost; ++s) {
+    double* out = other(cur);
+    sweep(h, l, cur, f, out);
+    cur = out;
+  }
+  if (cur != A)
+    CUDA_CHECK(cudaMemcpyAsync(A, cur, n * sizeof(double), cudaMemcpyDeviceToDevice,
+                               h->ctx->stream));
+}
+
+void sync_check(tpmg_hierarchy h) {
+  CUDA_CHECK(cudaStreamSynchronize(h->ctx->stream));
+  int err = 0;
+  CUDA_CHECK(cudaMemcpy(&err, h->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+  if (err) {
+    CUDA_CHECK(cudaMemset(h->d_err, 0, sizeof(int)));
+    throw Error(TPMG_E_SINGULAR, "thomas_solve: zero pivot");
+  }
+}
+
+double read_scalar(tpmg_hierarchy h, int slot) {
+  CUDA_CHECK(cudaMemcpyAsync(h->h_scal + slot, h->scal.p + slot, sizeof(double),
+                             cudaMemcpyDeviceToHost, h->ctx->stream));
+  sync_check(h);
+  return h->h_scal[slot];
+}
+
+tpmg_field_s* field_of(tpmg_field f) {
+  if (!f) throw Error(TPMG_E_CONFIG, "null field");
+  return f;
+}
+
+void same_hier(tpmg_hierarchy h, tpmg_field f) {
+  if (field_of(f)->h != h) throw Error(TPMG_E_SHAPE, "field belongs to another hierarchy");
+}
+
+// PCG iteration body (no host synchronisation): q = A p, p.q; x += a p, r -= a q, r.r;
+// z = V(r); r.z; p = z + b p.   Scalars: s[0]=rho, s[1]=p.q, s[2]=r.r, s[3]=rho_new.
+void pcg_iteration(tpmg_hierarchy h, double* x) {
+  const int L = h->finest();
+  const int64_t n = h->lv[L].plane * h->nz;
+  tpmg_context ctx = h->ctx;
+  apply_level(h, L, tpmg::APPLY_AU, h->p.p, nullptr, h->q.p, 1);
+  int nb = 0;
+  tpmg::launch_pcg_xr(ctx->launch(), n, h->scal.p, x, h->r.p, h->p.p, h->q.p, h->partials.p, &nb);
+  finish_dot(h, nb, 2);
+  vcycle(h, L, h->r.p, h->z.p, h->tmp.p, true);
+  dot_into(h, n, h->r.p, h->z.p, 3);
+  tpmg::launch_pcg_p(ctx->launch(), n, h->scal.p, h->z.p, h->p.p);
+  tpmg::launch_copy_scalar(ctx->launch(), h->scal.p, 0, 3);
+}
+
+void run_iteration(tpmg_hierarchy h, double* x) {
+  tpmg_context ctx = h->ctx;
+  if (!h->use_graphs) {
+    pcg_iteration(h, x);
+    return;
+  }
+  auto it = h->iter_graphs.find(x);
+  if (it == h->iter_graphs.end()) {
+    cudaGraph_t g;
+    const int64_t before = ctx->launches;
+    CUDA_CHECK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      pcg_iteration(h, x);
+    } catch (...) {
+      cudaStreamEndCapture(ctx->stream, &g);
+      throw;
+    }
+    CUDA_CHECK(cudaStreamEndCapture(ctx->stream, &g));
+    const int64_t nk = ctx->launches - before;
+    ctx->launches = before;
+    cudaGraphExec_t ge;
+    CUDA_CHECK(cudaGraphInstantiate(&ge, g, 0));
+    cudaGraphDestroy(g);
+    it = h->iter_graphs.emplace(x, ge).first;
+    h->iter_graph_kernels[x] = nk;
+  }
+  CUDA_CHECK(cudaGraphLaunch(it->second, ctx->stream));
+  ctx->launches += h->iter_graph_kernels[x];
+}
+
+}  // namespace
+
+// =========================================================================================
+extern "C" {
+
+const char* tpmg_status_string(int s) {
+  switch (s) {
+    case TPMG_OK: return "ok";
+    case TPMG_E_CONFIG: return "config_error";
+    case TPMG_E_SHAPE: return "shape_error";
+    case TPMG_E_NONFINITE: return "nonfinite_error";
+    case TPMG_E_FINGERPRINT: return "fingerprint_error";
+    case TPMG_E_SINGULAR: return "singular_error";
+    case TPMG_E_CAP: return "cap_error";
+    case TPMG_E_CUDA: return "cuda_error";
+    case TPMG_E_NCCL: return "nccl_error";
+    case TPMG_NOT_CONVERGED: return "not_converged";
+    case TPMG_BREAKDOWN: return "breakdown";
+    case TPMG_DIVERGED: return "diverged";
+    default: return "unknown";
+  }
+}
+
+int tpmg_abi_version(void) { return TPMG_ABI_VERSION; }
+
+int tpmg_nccl_unique_id(void* out128) {
+  return guard(nullptr, [&] {
+    g_nccl.load();
+    ncclUniqueId id;
+    NCCL_CHECK(g_nccl.GetUniqueId(&id));
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    std::memcpy(out128, &id, sizeof(id));
+  });
+}
+
+int tpmg_init(const tpmg_context_params* prm, tpmg_context* out) {
+  return guard(nullptr, [&] {
+    if (!prm || !out) throw Error(TPMG_E_CONFIG, "null argument");
+    if (prm->world_size < 1 || prm->rank < 0 || prm->rank >= prm->world_size)
+      throw Error(TPMG_E_CONFIG, "bad rank / world_size");
+    if (prm->px * prm->py != prm->world_size)
+      throw Error(TPMG_E_CONFIG, "process grid px*py must equal world_size");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      throw Error(TPMG_E_CUDA, "no CUDA device: the TPMG hot path has no CPU fallback");
+    auto ctx = std::make_unique<tpmg_context_s>();
+    if (prm->device >= 0) CUDA_CHECK(cudaSetDevice(prm->device));
+    CUDA_CHECK(cudaGetDevice(&ctx->device));
+    ctx->rank = prm->rank;
+    ctx->world = prm->world_size;
+    ctx->px = prm->px;
+    ctx->py = prm->py;
+    ctx->rx = prm->rank % prm->px;
+    ctx->ry = prm->rank / prm->px;
+    CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    if (ctx->world > 1) {
+      if (!prm->nccl_id) throw Error(TPMG_E_CONFIG, "world_size > 1 needs an ncclUniqueId");
+      g_nccl.load();
+      ncclUniqueId id;
+      std::memcpy(&id, prm->nccl_id, sizeof(id));
+      NCCL_CHECK(g_nccl.CommInitRank(&ctx->comm, ctx->world, id, ctx->rank));
+    }
+    *out = ctx.release();
+  });
+}
+
+int tpmg_finalize(tpmg_context ctx) {
+  if (!ctx) return TPMG_OK;
+  if (ctx->comm) g_nccl.CommDestroy(ctx->comm);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return TPMG_OK;
+}
+
+const char* tpmg_last_error(tpmg_context ctx) {
+  return ctx ? ctx->last_error.c_str() : g_global_error.c_str();
+}
+
+int tpmg_context_stream(tpmg_context ctx, void** stream) {
+  if (!ctx || !stream) return TPMG_E_CONFIG;
+  *stream = (void*)ctx->stream;
+  return TPMG_OK;
+}
+
+int tpmg_hier_create(tpmg_context ctx, const tpmg_grid_desc* g,
+                     const tpmg_factorized_profiles* p, double omega, const tpmg_mg_config* cfg,
+                     tpmg_hierarchy* out) {
+  return guard(ctx, [&] {
+    if (!ctx || !g || !p || !cfg || !out) throw Error(TPMG_E_CONFIG, "null argument");
+    CUDA_CHECK(cudaSetDevice(ctx->device));
+    const int64_t NX = g->nx, NY = g->ny, nz = g->nz;
+    if (NX < 1 || NY < 1 || nz < 1) throw Error(TPMG_E_CONFIG, "grid dimensions must be positive");
+    if (NX > (1 << 30) || NY > (1 << 30) || nz > (1 << 20))
+      throw Error(TPMG_E_CONFIG, "grid dimensions too large");
+    if (!(g->hx > 0.0) || !(g->hy > 0.0)) throw Error(TPMG_E_CONFIG, "cell widths must be positive");
+    if (cfg->smoother != TPMG_SMOOTHER_BLOCK_JACOBI)
+      throw Error(TPMG_E_CONFIG, "only the block_jacobi line smoother is data parallel");
+    if (!(cfg->relax > 0.0 && cfg->relax < 2.0))
+      throw Error(TPMG_E_CONFIG, "smoother relaxation factor must lie in (0, 2)");
+    if (cfg->nu_pre < 0 || cfg->nu_post < 0) throw Error(TPMG_E_CONFIG, "negative sweep count");
+    if (NX % ctx->px || NY % ctx->py)
+      throw Error(TPMG_E_CONFIG, "global grid does not split evenly over the process grid");
+    check_finite(g->z_faces, nz + 1, "z_faces");
+    for (int64_t k = 0; k < nz; ++k)
+      if (!(g->z_faces[k + 1] > g->z_faces[k]))
+        throw Error(TPMG_E_CONFIG, "vertical faces must increase");
+    const int64_t ncf = NX * NY;
+    check_finite(p->beta_r, nz, "beta_r");
+    check_finite(p->alpha_s_r, nz, "alpha_s_r");
+    check_finite(p->alpha_r_r, nz + 1, "alpha_r_r");
+    if (p->xi_r_r) check_finite(p->xi_r_r, nz + 1, "xi_r_r");
+    check_finite(p->beta_s, ncf, "beta_s");
+    check_finite(p->alpha_r_s, ncf, "alpha_r_s");
+    if (p->xi_r_s) check_finite(p->xi_r_s, ncf, "xi_r_s");
+    check_finite(p->alpha_s_s, 2 * ncf, "alpha_s_s");
+
+    // levels: tiles must stay even so the 2x2 children of a coarse cell share a rank
+    int levels = 1;
+    {
+      int64_t a = NX / ctx->px, b = NY / ctx->py, ga = NX, gb = NY;
+      if (cfg->depth <= 0) {
+        while (a % 2 == 0 && b % 2 == 0 && ga / 2 >= 4 && gb / 2 >= 4) {
+          a /= 2; b /= 2; ga /= 2; gb /= 2; ++levels;
+        }
+      } else {
+        for (int l = 1; l < cfg->depth; ++l) {
+          if (a % 2 || b % 2)
+            throw Error(TPMG_E_CONFIG, "tile does not coarsen to the requested depth");
+          a /= 2; b /= 2; ga /= 2; gb /= 2;
+        }
+        levels = cfg->depth;
+      }
+      if (cfg->prolongation == TPMG_PROLONG_LINEAR || cfg->restriction == TPMG_RESTRICT_TRANSPOSE)
+        if (levels > 1 && (ga < 3 || gb < 3))
+          throw Error(TPMG_E_CONFIG, "linear transfers need >= 3 coarse cells per dimension");
+    }
+
+    auto h = std::make_unique<tpmg_hierarchy_s>();
+    h->ctx = ctx;
+    h->nz = (int)nz;
+    h->xi = p->xi_r_r != nullptr && p->xi_r_s != nullptr;
+    h->relax = cfg->relax;
+    h->prolongation = cfg->prolongation;
+    h->restriction = cfg->restriction;
+    h->lv.resize(levels);
+    h->nu_pre.assign(levels, cfg->nu_pre);
+    h->nu_post.assign(levels, cfg->nu_post);
+    h->nu_pre[0] = 1;  // multigrid.hpp:269-270
+    h->nu_post[0] = 0;
+
+    // vertical hatted vectors (discretization.hpp:165-181, flat: volumes dz_k, r_k^2 -> 1)
+    const double* z = g->z_faces;
+    h->bv.resize(nz); h->sv.resize(nz); h->av.assign(nz + 1, 0.0); h->xv.assign(nz + 1, 0.0);
+    for (int64_t k = 0; k < nz; ++k) {
+      h->bv[k] = (z[k + 1] - z[k]) * p->beta_r[k];
+      h->sv[k] = (z[k + 1] - z[k]) * p->alpha_s_r[k];
+    }
+    for (int64_t k = 0; k <= nz; ++k) {
+      const double fd = (k >= 1 && k < nz) ? 2.0 / (z[k + 1] - z[k - 1]) : 0.0;
+      const double fa = (k >= 1 && k < nz) ? (z[k + 1] - z[k]) / (z[k + 1] - z[k - 1]) : 0.0;
+      h->av[k] = fd * p->alpha_r_r[k];
+      if (h->xi) h->xv[k] = fa * p->xi_r_r[k];
+    }
+    const double w2 = omega * omega;
+
+    // horizontal profiles on the current (global) level, restricted level by level
+    std::vector<double> pb(p->beta_s, p->beta_s + ncf), pa(p->alpha_r_s, p->alpha_r_s + ncf);
+    std::vector<double> px(ncf, 0.0), ps(p->alpha_s_s, p->alpha_s_s + 2 * ncf);
+    if (h->xi) px.assign(p->xi_r_s, p->xi_r_s + ncf);
+    int64_t gx = NX, gy = NY;
+    double hx = g->hx, hy = g->hy;
+    for (int l = levels - 1; l >= 0; --l) {
+      Level& L = h->lv[l];
+      L.gnx = (int)gx; L.gny = (int)gy;
+      L.nx = (int)(gx / ctx->px); L.ny = (int)(gy / ctx->py);
+      L.x0 = ctx->rx * L.nx; L.y0 = ctx->ry * L.ny;
+      L.plane = (int64_t)L.nx * L.ny;
+      const int64_t gnc = gx * gy;
+      // assemble_hatted (factorised), discretization.hpp:256-274, flat Cartesian geometry
+      const double area = hx * hy, ge_e = hy / hx, ge_n = hx / hy;
+      L.bh.resize(L.plane); L.ah.resize(L.plane); L.xh.resize(L.plane); L.sh.resize(2 * L.plane);
+      std::vector<double> sw(L.plane), se(L.plane), ss(L.plane), sn(L.plane);
+      for (int j = 0; j < L.ny; ++j)
+        for (int i = 0; i < L.nx; ++i) {
+          const int64_t c = (int64_t)j * L.nx + i;
+          const int64_t gi = L.x0 + i, gj = L.y0 + j, G = gj * gx + gi;
+          L.bh[c] = area * pb[G];
+          L.ah[c] = w2 * (area * pa[G]);
+          L.xh[c] = w2 * (area * px[G]);
+          const int64_t gw = gj * gx + (gi + gx - 1) % gx;
+          const int64_t gs = ((gj + gy - 1) % gy) * gx + gi;
+          L.sh[c] = w2 * ge_e * ps[G];
+          L.sh[L.plane + c] = w2 * ge_n * ps[gnc + G];
+          se[c] = L.sh[c];
+          sn[c] = L.sh[L.plane + c];
+          sw[c] = w2 * ge_e * ps[gw];
+          ss[c] = w2 * ge_n * ps[gnc + gs];
+        }
+      L.d_bh.upload(L.bh.data(), L.plane);
+      L.d_ah.upload(L.ah.data(), L.plane);
+      L.d_xh.upload(L.xh.data(), L.plane);
+      L.d_sw.upload(sw.data(), L.plane);
+      L.d_se.upload(se.data(), L.plane);
+      L.d_ss.upload(ss.data(), L.plane);
+      L.d_sn.upload(sn.data(), L.plane);
+      if (l == 0) break;
+      // restrict_profiles (factorised), multigrid.hpp:158-201: area-weighted mean of the 4
+      // children (:108-124), mean of the 2 co-linear child edges (:135-143)
+      const int64_t cx = gx / 2, cy = gy / 2, cnc = cx * cy;
+      std::vector<double> qb(cnc), qa(cnc), qx(cnc), qs(2 * cnc);
+      const double wf = hx * hy;
+      for (int64_t J = 0; J < cy; ++J)
+        for (int64_t I = 0; I < cx; ++I) {
+          const int64_t T = J * cx + I;
+          const int64_t c0 = (2 * J) * gx + 2 * I, c1 = c0 + 1, c2 = c0 + gx, c3 = c2 + 1;
+          auto mean4 = [&](const std::vector<double>& v) {
+            double acc = 0.0, ws = 0.0;
+            acc += wf * v[c0]; ws += wf;
+            acc += wf * v[c1]; ws += wf;
+            acc += wf * v[c2]; ws += wf;
+            acc += wf * v[c3]; ws += wf;
+            return acc / ws;
+          };
+          qb[T] = mean4(pb);
+          qa[T] = mean4(pa);
+          qx[T] = mean4(px);
+          qs[T] = (ps[c1] + ps[c3]) / 2.0;
+          qs[cnc + T] = (ps[gnc + c2] + ps[gnc + c3]) / 2.0;
+        }
+      pb.swap(qb); pa.swap(qa); px.swap(qx); ps.swap(qs);
+      gx = cx; gy = cy;
+      hx *= 2.0; hy *= 2.0;
+    }
+    h->d_bv.upload(h->bv.data(), nz);
+    h->d_sv.upload(h->sv.data(), nz);
+    h->d_av.upload(h->av.data(), nz + 1);
+    h->d_xv.upload(h->xv.data(), nz + 1);
+
+    // work buffers
+    int64_t max_blocks = 1024;
+    for (int l = 0; l < levels; ++l) {
+      Level& L = h->lv[l];
+      const int64_t n = L.plane * nz;
+      if (l < levels - 1) {
+        L.t.alloc(n);
+        L.u.alloc(n);
+        L.f.alloc(n);
+      }
+      if (ctx->world > 1) {
+        const int64_t faces = 2 * (int64_t)L.ny * nz + 2 * (int64_t)L.nx * nz;
+        L.send.alloc(faces);
+        L.recv.alloc(faces);
+      }
+      max_blocks = std::max<int64_t>(max_blocks, (L.plane + 255) / 256 + 1);
+    }
+    const int64_t nf = h->lv[levels - 1].plane * nz;
+    h->r.alloc(nf); h->z.alloc(nf); h->p.alloc(nf); h->q.alloc(nf); h->tmp.alloc(nf);
+    h->partials.alloc(std::max<int64_t>(max_blocks, 148 * 8));
+    h->scal.alloc(8);
+    CUDA_CHECK(cudaMemset(h->scal.p, 0, 8 * sizeof(double)));
+    CUDA_CHECK(cudaMalloc(&h->d_err, sizeof(int)));
+    CUDA_CHECK(cudaMemset(h->d_err, 0, sizeof(int)));
+    CUDA_CHECK(cudaMallocHost(&h->h_scal, 8 * sizeof(double)));
+    *out = h.release();
+  });
+}
+
+int tpmg_hier_destroy(tpmg_hierarchy h) {
+  if (!h) return TPMG_OK;
+  cudaStreamSynchronize(h->ctx->stream);
+  delete h;
+  return TPMG_OK;
+}
+
+int tpmg_hier_n_levels(tpmg_hierarchy h, int* n) {
+  return guard(h ? h->ctx : nullptr, [&] { *n = (int)h->lv.size(); });
+}
+
+int tpmg_hier_level_shape(tpmg_hierarchy h, int level, int64_t* nx, int64_t* ny, int64_t* nz,
+                          int64_t* x0, int64_t* y0) {
+  return guard(h->ctx, [&] {
+    if (level < 0 || level >= (int)h->lv.size()) throw Error(TPMG_E_SHAPE, "level out of range");
+    const Level& L = h->lv[level];
+    if (nx) *nx = L.nx;
+    if (ny) *ny = L.ny;
+    if (nz) *nz = h->nz;
+    if (x0) *x0 = L.x0;
+    if (y0) *y0 = L.y0;
+  });
+}
+
+int tpmg_hier_get_coefficients(tpmg_hierarchy h, int level, double* bh, double* ah, double* xh,
+                               double* sh, double* bv, double* sv, double* av, double* xv) {
+  return guard(h->ctx, [&] {
+    if (level < 0 || level >= (int)h->lv.size()) throw Error(TPMG_E_SHAPE, "level out of range");
+    const Level& L = h->lv[level];
+    const size_t np = L.plane * sizeof(double);
+    if (bh) std::memcpy(bh, L.bh.data(), np);
+    if (ah) std::memcpy(ah, L.ah.data(), np);
+    if (xh) std::memcpy(xh, L.xh.data(), np);
+    if (sh) std::memcpy(sh, L.sh.data(), 2 * np);
+    if (bv) std::memcpy(bv, h->bv.data(), h->nz * sizeof(double));
+    if (sv) std::memcpy(sv, h->sv.data(), h->nz * sizeof(double));
+    if (av) std::memcpy(av, h->av.data(), (h->nz + 1) * sizeof(double));
+    if (xv) std::memcpy(xv, h->xv.data(), (h->nz + 1) * sizeof(double));
+  });
+}
+
+int tpmg_field_create(tpmg_hierarchy h, int level, tpmg_field* out) {
+  return guard(h ? h->ctx : nullptr, [&] {
+    if (level < 0 || level >= (int)h->lv.size()) throw Error(TPMG_E_SHAPE, "level out of range");
+    auto f = std::make_unique<tpmg_field_s>();
+    f->h = h;
+    f->level = level;
+    f->buf.alloc(h->lv[level].plane * h->nz);
+    CUDA_CHECK(cudaMemsetAsync(f->buf.p, 0, f->buf.n * sizeof(double), h->ctx->stream));
+    CUDA_CHECK(cudaStreamSynchronize(h->ctx->stream));
+    *out = f.release();
+  });
+}
+
+int tpmg_field_destroy(tpmg_field f) {
+  if (f) {
+    cudaStreamSynchronize(f->h->ctx->stream);
+    delete f;
+  }
+  return TPMG_OK;
+}
+
+int tpmg_field_level(tpmg_field f, int* level) {
+  *level = f->level;
+  return TPMG_OK;
+}
+
+int tpmg_field_upload(tpmg_field f, const double* host, int layout) {
+  return guard(f->h->ctx, [&] {
+    tpmg_hierarchy h = f->h;
+    const int64_t n = f->buf.n;
+    cudaStream_t s = h->ctx->stream;
+    if (layout == TPMG_LAYOUT_X_FASTEST) {
+      CUDA_CHECK(cudaMemcpyAsync(f->buf.p, host, n * 8, cudaMemcpyHostToDevice, s));
+    } else if (layout == TPMG_LAYOUT_K_FASTEST) {
+      CUDA_CHECK(cudaMemcpyAsync(h->tmp.p, host, n * 8, cudaMemcpyHostToDevice, s));
+      tpmg::launch_kfast_to_xfast(h->ctx->launch(), h->lv[f->level].plane, h->nz, h->tmp.p,
+                                  f->buf.p);
+    } else {
+      throw Error(TPMG_E_CONFIG, "unknown layout");
+    }
+    CUDA_CHECK(cudaStreamSynchronize(s));
+  });
+}
+
+int tpmg_field_download(tpmg_field f, double* host, int layout) {
+  return guard(f->h->ctx, [&] {
+    tpmg_hierarchy h = f->h;
+    const int64_t n = f->buf.n;
+    cudaStream_t s = h->ctx->stream;
+    if (layout == TPMG_LAYOUT_X_FASTEST) {
+      CUDA_CHECK(cudaMemcpyAsync(host, f->buf.p, n * 8, cudaMemcpyDeviceToHost, s));
+    } else if (layout == TPMG_LAYOUT_K_FASTEST) {
+      tpmg::launch_xfast_to_kfast(h->ctx->launch(), h->lv[f->level].plane, h->nz, f->buf.p,
+                                  h->tmp.p);
+      CUDA_CHECK(cudaMemcpyAsync(host, h->tmp.p, n * 8, cudaMemcpyDeviceToHost, s));
+    } else {
+      throw Error(TPMG_E_CONFIG, "unknown layout");
+    }
+    CUDA_CHECK(cudaStreamSynchronize(s));
+  });
+}
+
+int tpmg_field_fill(tpmg_field f, double v) {
+  return guard(f->h->ctx, [&] {
+    fill(f->h, f->buf.p, f->buf.n, v);
+    sync_check(f->h);
+  });
+}
+
+int tpmg_field_copy(tpmg_field dst, tpmg_field src) {
+  return guard(dst->h->ctx, [&] {
+    if (dst->h != src->h || dst->level != src->level)
+      throw Error(TPMG_E_SHAPE, "field_copy: shapes differ");
+    CUDA_CHECK(cudaMemcpyAsync(dst->buf.p, src->buf.p, dst->buf.n * 8, cudaMemcpyDeviceToDevice,
+                               dst->h->ctx->stream));
+    sync_check(dst->h);
+  });
+}
+
+int tpmg_field_device_ptr(tpmg_field f, double** out) {
+  *out = f->buf.p;
+  return TPMG_OK;
+}
+
+int tpmg_apply(tpmg_hierarchy h, tpmg_field u, tpmg_field y) {
+  return guard(h->ctx, [&] {
+    same_hier(h, u);
+    same_hier(h, y);
+    if (u->level != y->level || u == y)
+      throw Error(TPMG_E_SHAPE, "apply_operator: field does not match the coefficients");
+    apply_level(h, u->level, tpmg::APPLY_AU, u->buf.p, nullptr, y->buf.p);
+    sync_check(h);
+  });
+}
+
+int tpmg_residual(tpmg_hierarchy h, tpmg_field f, tpmg_field u, tpmg_field r) {
+  return guard(h->ctx, [&] {
+    same_hier(h, f); same_hier(h, u); same_hier(h, r);
+    if (f->level != u->level || r->level != u->level || r == u)
+      throw Error(TPMG_E_SHAPE, "residual: field shapes do not match");
+    apply_level(h, u->level, tpmg::APPLY_RESID, u->buf.p, f->buf.p, r->buf.p);
+    sync_check(h);
+  });
+}
+
+int tpmg_smooth(tpmg_hierarchy h, tpmg_field u, tpmg_field f, int sweeps) {
+  return guard(h->ctx, [&] {
+    same_hier(h, u); same_hier(h, f);
+    if (u->level != f->level) throw Error(TPMG_E_SHAPE, "smooth: field shapes do not match");
+    if (!(h->relax > 0.0 && h->relax < 2.0))
+      throw Error(TPMG_E_CONFIG, "smoother relaxation factor must lie in (0, 2)");
+    const int l = u->level;
+    Level& L = h->lv[l];
+    double* A = u->buf.p;
+    double* B = (l == h->finest()) ? h->tmp.p : L.t.p;  // level scratch
+    double* cur = A;
+    for (int s = 0; s < sweeps; ++s) {
+      double* out = (cur == A) ? B : A;
+      sweep(h, l, cur, f->buf.p, out);
+      cur = out;
+    }
+    if (cur != A)
+      CUDA_CHECK(cudaMemcpyAsync(A, cur, u->buf.n * 8, cudaMemcpyDeviceToDevice, h->ctx->stream));
+    sync_check(h);
+  });
+}
+
+int tpmg_restrict(tpmg_hierarchy h, tpmg_field fine, tpmg_field coarse) {
+  return guard(h->ctx, [&] {
+    same_hier(h, fine); same_hier(h, coarse);
+    if (fine->level != coarse->level + 1)
+      throw Error(TPMG_E_SHAPE, "restrict_field: fine field is not one level above the target");
+    restrict_plain(h, fine->level, fine->buf.p, coarse->buf.p);
+    sync_check(h);
+  });
+}
+
+static int prolong_impl(tpmg_hierarchy h, tpmg_field coarse, tpmg_field fine, bool add) {
+  return guard(h->ctx, [&] {
+    same_hier(h, fine); same_hier(h, coarse);
+    if (fine->level != coarse->level + 1)
+      throw Error(TPMG_E_SHAPE, "prolongate_field: field level does not match");
+    prolong_level(h, coarse->level, coarse->buf.p, fine->buf.p, add);
+    sync_check(h);
+  });
+}
+
+int tpmg_prolong_add(tpmg_hierarchy h, tpmg_field coarse, tpmg_field fine) {
+  return prolong_impl(h, coarse, fine, true);
+}
+
+int tpmg_prolong(tpmg_hierarchy h, tpmg_field coarse, tpmg_field fine) {
+  return prolong_impl(h, coarse, fine, false);
+}
+
+int tpmg_vcycle(tpmg_hierarchy h, tpmg_field f, tpmg_field u) {
+  return guard(h->ctx, [&] {
+    same_hier(h, f); same_hier(h, u);
+    const int L = h->finest();
+    if (f->level != L || u->level != L) throw Error(TPMG_E_SHAPE, "v_cycle: fields must be finest");
+    vcycle(h, L, f->buf.p, u->buf.p, h->tmp.p, false);
+    sync_check(h);
+  });
+}
+
+int tpmg_dot(tpmg_hierarchy h, tpmg_field a, tpmg_field b, double* out) {
+  return guard(h->ctx, [&] {
+    same_hier(h, a); same_hier(h, b);
+    if (a->level != b->level) throw Error(TPMG_E_SHAPE, "dot: shapes differ");
+    dot_into(h, a->buf.n, a->buf.p, b->buf.p, 4);
+    *out = read_scalar(h, 4);
+  });
+}
+
+int tpmg_norm(tpmg_hierarchy h, tpmg_field a, double* out) {
+  double d = 0.0;
+  const int rc = tpmg_dot(h, a, a, &d);
+  if (rc == TPMG_OK) *out = std::sqrt(d);
+  return rc;
+}
+
+int tpmg_measure_cycle_rate(tpmg_hierarchy h, tpmg_field f, int n_cycles, double* rate) {
+  return guard(h->ctx, [&] {
+    same_hier(h, f);
+    const int L = h->finest();
+    if (f->level != L) throw Error(TPMG_E_SHAPE, "measure_cycle_rate: f must be finest");
+    if (n_cycles < 2) throw Error(TPMG_E_CONFIG, "measure_cycle_rate needs at least two cycles");
+    const int64_t n = f->buf.n;
+    double* u = h->z.p;
+    double* r = h->r.p;
+    fill(h, u, n, 0.0);
+    double first = 0.0, last = 0.0;
+    for (int i = 1; i <= n_cycles; ++i) {
+      vcycle(h, L, f->buf.p, u, h->tmp.p, i == 1);
+      apply_level(h, L, tpmg::APPLY_RESID, u, f->buf.p, r);
+      dot_into(h, n, r, r, 5);
+      const double nrm = std::sqrt(read_scalar(h, 5));
+      if (i == 1) first = nrm;
+      last = nrm;
+    }
+    dot_into(h, n, f->buf.p, f->buf.p, 5);
+    const double fn = std::sqrt(read_scalar(h, 5));
+    if (first <= 1e-300 || first <= 2.220446049250313e-16 * fn) {
+      *rate = 0.0;
+      return;
+    }
+    *rate = std::pow(last / first, 1.0 / (double)(n_cycles - 1));
+  });
+}
+
+int tpmg_pcg(tpmg_hierarchy h, tpmg_field f, tpmg_field x, double tol, int max_iter,
+             double* res_hist, int* iters, int* solve_status) {
+  return guard(h->ctx, [&] {
+    same_hier(h, f); same_hier(h, x);
+    const int L = h->finest();
+    if (f->level != L || x->level != L) throw Error(TPMG_E_SHAPE, "pcg: fields must be finest");
+    if (max_iter < 0) throw Error(TPMG_E_CONFIG, "max_iter must be >= 0");
+    tpmg_context ctx = h->ctx;
+    const int64_t n = f->buf.n;
+    cudaStream_t s = ctx->stream;
+    CUDA_CHECK(cudaMemsetAsync(x->buf.p, 0, n * 8, s));
+    CUDA_CHECK(cudaMemcpyAsync(h->r.p, f->buf.p, n * 8, cudaMemcpyDeviceToDevice, s));
+    dot_into(h, n, h->r.p, h->r.p, 2);
+    const double r0 = std::sqrt(read_scalar(h, 2));
+    if (res_hist) res_hist[0] = r0;
+    *iters = 0;
+    *solve_status = TPMG_OK;
+    if (r0 == 0.0) return;
+    vcycle(h, L, h->r.p, h->z.p, h->tmp.p, true);
+    CUDA_CHECK(cudaMemcpyAsync(h->p.p, h->z.p, n * 8, cudaMemcpyDeviceToDevice, s));
+    dot_into(h, n, h->r.p, h->z.p, 0);
+    if (!(read_scalar(h, 0) > 0.0)) {
+      *solve_status = TPMG_BREAKDOWN;
+      return;
+    }
+    for (int it = 1; it <= max_iter; ++it) {
+      run_iteration(h, x->buf.p);
+      CUDA_CHECK(cudaMemcpyAsync(h->h_scal, h->scal.p, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
+      sync_check(h);
+      const double pq = h->h_scal[1], rr = h->h_scal[2], rho_new = h->h_scal[3];
+      if (!(pq > 0.0)) {
+        *solve_status = TPMG_BREAKDOWN;
+        return;
+      }
+      const double rn = std::sqrt(rr);
+      if (res_hist) res_hist[it] = rn;
+      *iters = it;
+      if (rn / r0 <= tol) return;
+      if (rn / r0 > 1e4) {
+        *solve_status = TPMG_DIVERGED;
+        return;
+      }
+      if (!(rho_new > 0.0)) {
+        *solve_status = TPMG_BREAKDOWN;
+        return;
+      }
+    }
+    *solve_status = TPMG_NOT_CONVERGED;
+  });
+}
+
+int tpmg_pcg_host(tpmg_hierarchy h, const double* f_host, double* x_host, int layout, double tol,
+                  int max_iter, double* res_hist, int* iters, int* solve_status) {
+  tpmg_field f = nullptr, x = nullptr;
+  int rc = tpmg_field_create(h, h->finest(), &f);
+  if (rc == TPMG_OK) rc = tpmg_field_create(h, h->finest(), &x);
+  if (rc == TPMG_OK) rc = tpmg_field_upload(f, f_host, layout);
+  if (rc == TPMG_OK) rc = tpmg_pcg(h, f, x, tol, max_iter, res_hist, iters, solve_status);
+  if (rc == TPMG_OK) rc = tpmg_field_download(x, x_host, layout);
+  tpmg_field_destroy(f);
+  tpmg_field_destroy(x);
+  return rc;
+}
+
+int tpmg_kernel_launch_count(tpmg_context ctx, int64_t* out) {
+  *out = ctx->launches;
+  return TPMG_OK;
+}
+
+int tpmg_time_kernel(tpmg_hierarchy h, int kernel_id, int level, int reps, double* avg_ms) {
+  return guard(h->ctx, [&] {
+    if (level < 0 || level >= (int)h->lv.size()) throw Error(TPMG_E_SHAPE, "level out of range");
+    if (reps < 1) throw Error(TPMG_E_CONFIG, "reps must be >= 1");
+    const bool transfer = kernel_id == TPMG_K_RESID_RESTRICT || kernel_id == TPMG_K_PROLONG_ADD ||
+                          kernel_id == TPMG_K_RESTRICT;
+    if (transfer && level < 1) throw Error(TPMG_E_SHAPE, "transfers need a fine level >= 1");
+    Level& L = h->lv[level];
+    const int64_t n = L.plane * h->nz;
+    DevBuf a, b, c, cc;
+    a.alloc(n); b.alloc(n); c.alloc(n);
+    const int64_t ncoarse = transfer ? h->lv[level - 1].plane * h->nz : 1;
+    cc.alloc(ncoarse);
+    tpmg::launch_fill(h->ctx->launch(), n, a.p, 0.5);
+    tpmg::launch_fill(h->ctx->launch(), n, b.p, 0.25);
+    tpmg::launch_fill(h->ctx->launch(), ncoarse, cc.p, 0.125);
+    auto once = [&] {
+      switch (kernel_id) {
+        case TPMG_K_APPLY: apply_level(h, level, tpmg::APPLY_AU, a.p, nullptr, c.p); break;
+        case TPMG_K_RESIDUAL: apply_level(h, level, tpmg::APPLY_RESID, a.p, b.p, c.p); break;
+        case TPMG_K_JACOBI: sweep(h, level, a.p, b.p, c.p); break;
+        case TPMG_K_JACOBI_ZERO: sweep(h, level, nullptr, b.p, c.p); break;
+        case TPMG_K_RESID_RESTRICT: resid_restrict(h, level, a.p, b.p, cc.p, c.p); break;
+        case TPMG_K_PROLONG_ADD: prolong_level(h, level - 1, cc.p, c.p, true); break;
+        case TPMG_K_RESTRICT: restrict_plain(h, level, a.p, cc.p); break;
+        default: throw Error(TPMG_E_CONFIG, "unknown kernel id");
+      }
+    };
+    once();  // warm-up
+    cudaEvent_t e0, e1;
+    CUDA_CHECK(cudaEventCreate(&e0));
+    CUDA_CHECK(cudaEventCreate(&e1));
+    CUDA_CHECK(cudaEventRecord(e0, h->ctx->stream));
+    for (int r = 0; r < reps; ++r) once();
+    CUDA_CHECK(cudaEventRecord(e1, h->ctx->stream));
+    CUDA_CHECK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    sync_check(h);
+    *avg_ms = ms / reps;
+  });
+}
+
+int tpmg_set_use_graphs(tpmg_hierarchy h, int enable) {
+  h->use_graphs = enable != 0;
+  return TPMG_OK;
+}
+
+}  // extern "C"

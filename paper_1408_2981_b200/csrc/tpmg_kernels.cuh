@@ -1,0 +1,106 @@
+// tpmg_kernels.cuh -- device data views and kernel launchers of the sm_100a hot path.
+//
+// Device layout of every field: [k][y][x], x fastest (the transpose of the reference's
+// k-fastest Field, discretization.hpp:106-120), so a warp covers 32 consecutive x columns
+// and every load/store at fixed k is coalesced.  Coefficients are the separable hatted
+// factors of discretization.hpp:32-67: four vertical vectors shared by all levels and six
+// per-column horizontal scalars (bh, ah, xh and the four edge scalars W,E,S,N), i.e. 48 B
+// per column, rebuilt into the column blocks on the fly (build_column, discretization.hpp:
+// 235-251).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tpmg {
+
+struct VertCoef {      // HattedComponent::vert of beta, alpha_s, alpha_r, xi_r
+  const double* bv;    // nz
+  const double* sv;    // nz
+  const double* av;    // nz+1
+  const double* xv;    // nz+1 (only read when the level has advection)
+};
+
+struct LevelCoef {     // HattedComponent::horiz, per column of the local tile
+  int nx, ny, nz;
+  int64_t plane;       // nx*ny
+  const double* bh;
+  const double* ah;
+  const double* xh;
+  const double* sw;    // alpha_s hat of the W / E / S / N edge of each column
+  const double* se;
+  const double* ss;
+  const double* sn;
+};
+
+// Where the neighbour values across each tile face live.  For direction d
+// (0=W,1=E,2=S,3=N) the value adjacent to boundary position t (t = y for W/E,
+// x for S/N) at level k is p[d][k*sk[d] + t*st[d]].  Single GPU: strided views of
+// the field itself (periodic wrap, no copy).  Multi GPU: NCCL-filled halo buffers.
+struct Halo {
+  const double* p[4];
+  int64_t sk[4];
+  int64_t st[4];
+};
+
+enum ApplyMode { APPLY_AU = 0, APPLY_RESID = 1 };
+
+// Deterministic reduction workspace: per-block partials, then one fixed-order pass.
+constexpr int kMaxPartials = 8192;
+
+struct Launch {
+  cudaStream_t stream;
+  int64_t* counter;  // incremented once per kernel launch (instrumentation)
+};
+
+Halo self_halo(const double* u, int nx, int ny, int64_t plane);
+
+// y = A u  (apply_operator, discretization.hpp:262-278)  or  y = f - A u.
+// If dot_partials != nullptr, per-block partial sums of y.u are written there (count returned
+// through *nblocks) for a fused p.q in PCG.
+void launch_apply(const Launch& L, const VertCoef& V, const LevelCoef& C, bool xi, int mode,
+                  const double* u, const Halo& H, const double* f, double* y,
+                  double* dot_partials, int* nblocks);
+
+// One block-Jacobi line sweep (smooth, relaxation.hpp:77-97): out = u + relax * T^{-1}(f - A u);
+// u == nullptr means a zero initial guess.  Zero pivots set bit 1 in *err.
+void launch_jacobi(const Launch& L, const VertCoef& V, const LevelCoef& C, bool xi,
+                   const double* u, const Halo& H, const double* f, double* out, double relax,
+                   int* err);
+
+// coarse = R_sum(fine) (restrict_field, multigrid.hpp:29-43).
+void launch_restrict_sum(const Launch& L, int cnx, int cny, int nz, const double* fine,
+                         double* coarse);
+// coarse = R_sum(f - A u) fused (multigrid.hpp:285-291), u on the fine level.
+void launch_resid_restrict_sum(const Launch& L, const VertCoef& V, const LevelCoef& Cf, bool xi,
+                               const double* u, const Halo& H, const double* f, double* coarse);
+// coarse = P^T fine (restrict_field_transpose, multigrid.hpp:46-69); Hf: fine face halo.
+void launch_restrict_transpose(const Launch& L, int cnx, int cny, int nz, const double* fine,
+                               const Halo& Hf, double* coarse);
+// fine (+)= P coarse (prolongate_field, multigrid.hpp:74-100; +=, :294-295); Hc: coarse halo.
+void launch_prolong(const Launch& L, int fnx, int fny, int nz, const double* coarse,
+                    const Halo& Hc, double* fine, bool linear, bool add);
+
+// PCG vector kernels (device scalars: s[0]=rho, s[1]=p.q, s[2]=r.r, s[3]=rho_new).
+// x += alpha p; r -= alpha q; partial |r|^2.   alpha = s[0]/s[1].
+void launch_pcg_xr(const Launch& L, int64_t n, const double* s, double* x, double* r,
+                   const double* p, const double* q, double* partials, int* nblocks);
+// p = z + beta p, beta = s[3]/s[0]; then s[0] = s[3] is done by the finaliser.
+void launch_pcg_p(const Launch& L, int64_t n, const double* s, const double* z, double* p);
+// partial dot a.b
+void launch_dot(const Launch& L, int64_t n, const double* a, const double* b, double* partials,
+                int* nblocks);
+// out[slot] = sum(partials[0..nblocks)) in fixed order; if copy_from >= 0 also s[copy_to] = s[copy_from]
+// first (used to roll rho_new -> rho).
+void launch_reduce(const Launch& L, const double* partials, int nblocks, double* out);
+void launch_copy_scalar(const Launch& L, double* s, int dst, int src);
+
+// Layout permutations for upload/download: k-fastest (reference Field) <-> [k][y][x].
+void launch_kfast_to_xfast(const Launch& L, int64_t ncol, int nz, const double* in, double* out);
+void launch_xfast_to_kfast(const Launch& L, int64_t ncol, int nz, const double* in, double* out);
+void launch_fill(const Launch& L, int64_t n, double* p, double v);
+
+// Multi-GPU halo packing: face values of u into send buffers [W|E|S|N] of sizes ny*nz,ny*nz,nx*nz,nx*nz.
+void launch_pack_faces(const Launch& L, int nx, int ny, int nz, const double* u, double* send);
+
+}  // namespace tpmg

@@ -1,0 +1,329 @@
+"""Host-side mirror of the reference's operator / smoother / transfer / solver interface.
+
+Function names and argument meaning follow the reference (proj/include/tpmg/):
+``apply_operator`` (discretization.hpp:262-287), ``smooth`` (relaxation.hpp:63-108),
+``restrict_field`` / ``restrict_field_transpose`` (multigrid.hpp:29-69),
+``prolongate_field`` (multigrid.hpp:74-100), ``build_hierarchy_coefficients``
+(multigrid.hpp:242-272), ``v_cycle`` (multigrid.hpp:276-299), ``measure_cycle_rate``
+(multigrid.hpp:302-321) plus the PCG driver of BASELINE.json.  Errors are raised as the
+reference's exception types (types.hpp:24-58).  Every call goes through the C-ABI of
+``libtpmg_b200.so`` into hand-written sm_100a kernels; nothing here computes.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import time
+
+import numpy as np
+
+from . import _capi
+from ._capi import ContextParams, FactorizedProfiles, GridDesc, MGConfig
+
+K_FASTEST, X_FASTEST = 0, 1
+K_APPLY, K_JACOBI, K_JACOBI_ZERO, K_RESID_RESTRICT, K_PROLONG_ADD, K_RESTRICT, K_RESIDUAL = range(7)
+LINEAR, INJECTION = 0, 1
+SUMMATION, TRANSPOSE = 0, 1
+OK, E_CONFIG, E_SHAPE, E_NONFINITE, E_FINGERPRINT, E_SINGULAR, E_CAP, E_CUDA, E_NCCL = range(9)
+NOT_CONVERGED, BREAKDOWN, DIVERGED = 9, 10, 11
+
+
+class TpmgError(RuntimeError):
+    code = -1
+
+
+class config_error(TpmgError):
+    code = E_CONFIG
+
+
+class shape_error(TpmgError):
+    code = E_SHAPE
+
+
+class nonfinite_error(TpmgError):
+    code = E_NONFINITE
+
+
+class fingerprint_error(TpmgError):
+    code = E_FINGERPRINT
+
+
+class singular_error(TpmgError):
+    code = E_SINGULAR
+
+
+class cap_error(TpmgError):
+    code = E_CAP
+
+
+class cuda_error(TpmgError):
+    code = E_CUDA
+
+
+class nccl_error(TpmgError):
+    code = E_NCCL
+
+
+_ERRORS = {c.code: c for c in (config_error, shape_error, nonfinite_error, fingerprint_error,
+                                singular_error, cap_error, cuda_error, nccl_error)}
+
+
+def _p(a: np.ndarray | None):
+    if a is None:
+        return None
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+class Context:
+    """One GPU (rank) -- tpmg_init / tpmg_finalize."""
+
+    def __init__(self, device: int = 0, rank: int = 0, world_size: int = 1, px: int = 1,
+                 py: int = 1, nccl_id: bytes | None = None, variant: str = "fast"):
+        self.lib = _capi.load(variant)
+        self._idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id else None
+        prm = ContextParams(device, rank, world_size, px, py,
+                            C.cast(self._idbuf, C.c_void_p) if self._idbuf else None)
+        h = C.c_void_p()
+        self._h = None
+        self._check(self.lib.tpmg_init(C.byref(prm), C.byref(h)))
+        self._h = h
+        self.rank, self.world_size, self.px, self.py = rank, world_size, px, py
+
+    def _check(self, rc: int):
+        if rc != OK:
+            msg = self.lib.tpmg_last_error(self._h if self._h else None)
+            raise _ERRORS.get(rc, TpmgError)(f"{self.lib.tpmg_status_string(rc).decode()}: "
+                                             f"{msg.decode() if msg else ''}")
+
+    @staticmethod
+    def nccl_unique_id(variant: str = "fast") -> bytes:
+        lib = _capi.load(variant)
+        buf = C.create_string_buffer(128)
+        rc = lib.tpmg_nccl_unique_id(buf)
+        if rc != OK:
+            raise nccl_error(lib.tpmg_last_error(None).decode())
+        return buf.raw
+
+    def stream_handle(self) -> int:
+        """cudaStream_t (as int) the library orders all work on."""
+        s = C.c_void_p()
+        self._check(self.lib.tpmg_context_stream(self._h, C.byref(s)))
+        return s.value or 0
+
+    def kernel_launches(self) -> int:
+        n = C.c_int64()
+        self.lib.tpmg_kernel_launch_count(self._h, C.byref(n))
+        return n.value
+
+    def close(self):
+        if self._h is not None:
+            self.lib.tpmg_finalize(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Field:
+    """Device-resident Field (discretization.hpp:106-120) of one level, stored [k][y][x]."""
+
+    def __init__(self, hier: "Hierarchy", level: int):
+        self.hier, self.level = hier, level
+        h = C.c_void_p()
+        hier.ctx._check(hier.lib.tpmg_field_create(hier._h, level, C.byref(h)))
+        self._h = h
+        self.nx, self.ny, self.nz = hier.level_shape(level)[:3]
+
+    @property
+    def size(self) -> int:
+        return self.nx * self.ny * self.nz
+
+    def upload(self, a: np.ndarray, layout: int = X_FASTEST) -> "Field":
+        a = np.ascontiguousarray(a, dtype=np.float64).reshape(-1)
+        if a.size != self.size:
+            raise shape_error(f"upload: {a.size} values for a field of {self.size}")
+        self.hier.ctx._check(self.hier.lib.tpmg_field_upload(self._h, _p(a), layout))
+        return self
+
+    def download(self, layout: int = X_FASTEST) -> np.ndarray:
+        out = np.empty(self.size, dtype=np.float64)
+        self.hier.ctx._check(self.hier.lib.tpmg_field_download(self._h, _p(out), layout))
+        return out.reshape(self.nz, self.ny, self.nx) if layout == X_FASTEST else out
+
+    def fill(self, v: float) -> "Field":
+        self.hier.ctx._check(self.hier.lib.tpmg_field_fill(self._h, C.c_double(v)))
+        return self
+
+    def copy_from(self, other: "Field") -> "Field":
+        self.hier.ctx._check(self.hier.lib.tpmg_field_copy(self._h, other._h))
+        return self
+
+    def norm(self) -> float:
+        out = C.c_double()
+        self.hier.ctx._check(self.hier.lib.tpmg_norm(self.hier._h, self._h, C.byref(out)))
+        return out.value
+
+    def close(self):
+        if getattr(self, "_h", None) is not None:
+            self.hier.lib.tpmg_field_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Hierarchy:
+    """MultigridHierarchy built by build_hierarchy_coefficients (multigrid.hpp:242-272)."""
+
+    def __init__(self, ctx: Context, problem, **over):
+        self.ctx, self.lib = ctx, ctx.lib
+        P = problem
+        kw = P.mg_kwargs()
+        kw.update(over)
+        self._keep = [np.ascontiguousarray(a, dtype=np.float64) for a in
+                      (P.z_faces, P.beta_r, P.alpha_s_r, P.alpha_r_r, P.beta_s, P.alpha_r_s,
+                       P.alpha_s_s)]
+        z, br, asr, arr, bs, ars, ass = self._keep
+        grid = GridDesc(P.nx, P.ny, P.hx, P.hy, P.nz, _p(z))
+        prof = FactorizedProfiles(_p(br), _p(asr), _p(arr), None, _p(bs), _p(ars), None, _p(ass))
+        cfg = MGConfig(kw.get("smoother", 0), kw["relax"], kw["prolongation"], kw["restriction"],
+                       kw["nu_pre"], kw["nu_post"], kw["depth"])
+        h = C.c_void_p()
+        self._h = None
+        ctx._check(self.lib.tpmg_hier_create(ctx._h, C.byref(grid), C.byref(prof),
+                                             C.c_double(P.omega), C.byref(cfg), C.byref(h)))
+        self._h = h
+        self._keep = None
+        self.problem = P
+        n = C.c_int()
+        self.lib.tpmg_hier_n_levels(self._h, C.byref(n))
+        self.n_levels = n.value
+        self.finest = self.n_levels - 1
+
+    def level_shape(self, level: int):
+        v = [C.c_int64() for _ in range(5)]
+        self.ctx._check(self.lib.tpmg_hier_level_shape(self._h, level, *[C.byref(x) for x in v]))
+        return tuple(x.value for x in v)  # nx, ny, nz, x0, y0
+
+    def field(self, level: int | None = None) -> Field:
+        return Field(self, self.finest if level is None else level)
+
+    def coefficients(self, level: int) -> dict:
+        nx, ny, nz = self.level_shape(level)[:3]
+        nc = nx * ny
+        out = dict(bh=np.empty(nc), ah=np.empty(nc), xh=np.empty(nc), sh=np.empty(2 * nc),
+                   bv=np.empty(nz), sv=np.empty(nz), av=np.empty(nz + 1), xv=np.empty(nz + 1))
+        self.ctx._check(self.lib.tpmg_hier_get_coefficients(
+            self._h, level, *[_p(out[k]) for k in ("bh", "ah", "xh", "sh", "bv", "sv", "av", "xv")]))
+        return out
+
+    def time_kernel(self, kernel_id: int, level: int | None = None, reps: int = 20) -> float:
+        """Average device milliseconds per launch (tpmg_time_kernel)."""
+        out = C.c_double()
+        self.ctx._check(self.lib.tpmg_time_kernel(self._h, kernel_id,
+                                                  self.finest if level is None else level, reps,
+                                                  C.byref(out)))
+        return out.value
+
+    def set_use_graphs(self, on: bool):
+        self.lib.tpmg_set_use_graphs(self._h, 1 if on else 0)
+
+    def close(self):
+        if getattr(self, "_h", None) is not None:
+            self.lib.tpmg_hier_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---- reference-shaped free functions ----------------------------------------------------------
+
+def build_hierarchy_coefficients(ctx: Context, problem, **over) -> Hierarchy:
+    return Hierarchy(ctx, problem, **over)
+
+
+def apply_operator(h: Hierarchy, u: Field, out: Field) -> Field:
+    h.ctx._check(h.lib.tpmg_apply(h._h, u._h, out._h))
+    return out
+
+
+def residual(h: Hierarchy, f: Field, u: Field, r: Field) -> Field:
+    h.ctx._check(h.lib.tpmg_residual(h._h, f._h, u._h, r._h))
+    return r
+
+
+def smooth(h: Hierarchy, u: Field, f: Field, sweeps: int) -> Field:
+    h.ctx._check(h.lib.tpmg_smooth(h._h, u._h, f._h, sweeps))
+    return u
+
+
+def restrict_field(h: Hierarchy, fine: Field, coarse: Field) -> Field:
+    h.ctx._check(h.lib.tpmg_restrict(h._h, fine._h, coarse._h))
+    return coarse
+
+
+def prolongate_field(h: Hierarchy, coarse: Field, fine: Field, add: bool = False) -> Field:
+    fn = h.lib.tpmg_prolong_add if add else h.lib.tpmg_prolong
+    h.ctx._check(fn(h._h, coarse._h, fine._h))
+    return fine
+
+
+def v_cycle(h: Hierarchy, f: Field, u: Field) -> Field:
+    h.ctx._check(h.lib.tpmg_vcycle(h._h, f._h, u._h))
+    return u
+
+
+def measure_cycle_rate(h: Hierarchy, f: Field, n_cycles: int) -> float:
+    out = C.c_double()
+    h.ctx._check(h.lib.tpmg_measure_cycle_rate(h._h, f._h, n_cycles, C.byref(out)))
+    return out.value
+
+
+def dot(h: Hierarchy, a: Field, b: Field) -> float:
+    out = C.c_double()
+    h.ctx._check(h.lib.tpmg_dot(h._h, a._h, b._h, C.byref(out)))
+    return out.value
+
+
+class SolveResult:
+    def __init__(self, iters, status, history, seconds):
+        self.iterations, self.status, self.history, self.seconds = iters, status, history, seconds
+
+    @property
+    def converged(self) -> bool:
+        return self.status == OK
+
+    def __repr__(self):
+        return (f"SolveResult(iterations={self.iterations}, status={self.status}, "
+                f"rel_res={self.history[-1] / self.history[0] if len(self.history) else None})")
+
+
+def pcg_solve(h: Hierarchy, f: Field, x: Field, tol: float, max_iter: int = 500) -> SolveResult:
+    hist = np.zeros(max_iter + 1)
+    it, st = C.c_int(), C.c_int()
+    t0 = time.perf_counter()
+    h.ctx._check(h.lib.tpmg_pcg(h._h, f._h, x._h, C.c_double(tol), max_iter, _p(hist),
+                                C.byref(it), C.byref(st)))
+    return SolveResult(it.value, st.value, hist[: it.value + 1].copy(), time.perf_counter() - t0)
+
+
+def pcg_solve_host(h: Hierarchy, f_host: np.ndarray, tol: float, max_iter: int = 500,
+                   layout: int = X_FASTEST):
+    """End-to-end: host f -> device -> PCG -> host x (tpmg_pcg_host)."""
+    f_host = np.ascontiguousarray(f_host, dtype=np.float64).reshape(-1)
+    x = np.empty_like(f_host)
+    hist = np.zeros(max_iter + 1)
+    it, st = C.c_int(), C.c_int()
+    h.ctx._check(h.lib.tpmg_pcg_host(h._h, _p(f_host), _p(x), layout, C.c_double(tol), max_iter,
+                                     _p(hist), C.byref(it), C.byref(st)))
+    return x, SolveResult(it.value, st.value, hist[: it.value + 1].copy(), 0.0)
