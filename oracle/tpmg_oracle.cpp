@@ -73,6 +73,7 @@ struct Hier {
   int prolongation = 0, restriction = 0;
   std::vector<int> nu_pre, nu_post;
   int threads = 1;
+  Index cart_nx = 0, cart_ny = 0;  // finest Cartesian dims (0 for generic tables)
 };
 
 // ColumnMatrix, discretization.hpp:208-231.
@@ -290,6 +291,95 @@ double dot(Index n, const double* a, const double* b) {
   return nch ? part[0] : 0.0;
 }
 
+// ---- device reduction order ------------------------------------------------------------
+// The GPU path reduces dot products with a fixed tree (paper_1408_2981_b200/csrc/
+// tpmg_kernels.cu: block_sum, k_dot, k_pcg_xr, k_reduce, k_apply[_tiled]).  The oracle's
+// PCG uses the same tree so that the strict GPU build can be compared bitwise end to end;
+// the reference's own summation order (Eigen's vectorised norm, discretization.hpp:27) is
+// not pinned by any reference test.
+double warp_tree(double* v) {  // __shfl_down_sync tree, result of lane 0
+  for (int o = 16; o > 0; o >>= 1)
+    for (int i = 0; i < o; ++i) v[i] = v[i] + v[i + o];
+  return v[0];
+}
+
+double block_tree(const double* acc, int nthreads) {  // block_sum
+  double part[32];
+  const int nw = (nthreads + 31) / 32;
+  for (int w = 0; w < nw; ++w) {
+    double v[32];
+    for (int l = 0; l < 32; ++l) v[l] = acc[w * 32 + l];
+    part[w] = warp_tree(v);
+  }
+  double v[32];
+  for (int l = 0; l < 32; ++l) v[l] = l < nw ? part[l] : 0.0;
+  return warp_tree(v);
+}
+
+double reduce_partials(const std::vector<double>& p) {  // k_reduce<<<1,1024>>>
+  std::vector<double> acc(1024, 0.0);
+  for (int t = 0; t < 1024; ++t)
+    for (size_t q = t; q < p.size(); q += 1024) acc[t] += p[q];
+  return block_tree(acc.data(), 1024);
+}
+
+// Layout of the finest level on the device: [k][y][x]; element t <-> oracle (col, k).
+struct DevOrder {
+  Index nx = 0, ny = 0, nz = 0;
+  Index plane() const { return nx * ny; }
+  Index oidx(Index t) const { return (t % plane()) * nz + t / plane(); }
+};
+
+// k_dot / k_pcg_xr: grid-stride over the x-fastest index with vec_blocks(n) blocks of 256.
+template <typename Val>
+double gridstride_dot(const DevOrder& d, Val val) {
+  const Index n = d.plane() * d.nz;
+  Index B = (n + 255) / 256;
+  if (B > 148 * 8) B = 148 * 8;
+  if (B < 1) B = 1;
+  const Index G = B * 256;
+  std::vector<double> acc(G, 0.0);
+  for (Index g = 0; g < G; ++g) {
+    double a = 0.0;
+    for (Index t = g; t < n; t += G) a += val(d.oidx(t));
+    acc[g] = a;
+  }
+  std::vector<double> part(B);
+  for (Index b = 0; b < B; ++b) part[b] = block_tree(acc.data() + b * 256, 256);
+  return reduce_partials(part);
+}
+
+// fused p.q of the apply kernel: per-column sums over k, then per-CTA trees.
+double column_dot(const DevOrder& d, const double* y, const double* u) {
+  const Index plane = d.plane();
+  std::vector<double> colsum(plane);
+  for (Index c = 0; c < plane; ++c) {
+    double a = 0.0;
+    for (Index k = 0; k < d.nz; ++k) a += y[c * d.nz + k] * u[c * d.nz + k];
+    colsum[c] = a;
+  }
+  std::vector<double> part;
+  if (d.nx % 32 == 0 && d.ny % 4 == 0) {  // k_apply_tiled: 32x4 tiles, tile order by*gx+bx
+    const Index gx = d.nx / 32, gy = d.ny / 4;
+    part.resize(gx * gy);
+    double acc[128];
+    for (Index by = 0; by < gy; ++by)
+      for (Index bx = 0; bx < gx; ++bx) {
+        for (int t = 0; t < 128; ++t) acc[t] = colsum[(by * 4 + t / 32) * d.nx + bx * 32 + t % 32];
+        part[by * gx + bx] = block_tree(acc, 128);
+      }
+  } else {  // k_apply: 256 consecutive columns per block
+    const Index B = (plane + 255) / 256;
+    part.resize(B);
+    double acc[256];
+    for (Index b = 0; b < B; ++b) {
+      for (int t = 0; t < 256; ++t) acc[t] = b * 256 + t < plane ? colsum[b * 256 + t] : 0.0;
+      part[b] = block_tree(acc, 256);
+    }
+  }
+  return reduce_partials(part);
+}
+
 void check_finite(const double* p, Index n, const char* what) {
   for (Index i = 0; i < n; ++i)
     if (!std::isfinite(p[i])) throw Error(E_NONFINITE, std::string("non-finite values in ") + what);
@@ -378,6 +468,8 @@ int tpmgo_cart_create(int64_t nx, int64_t ny, double hx, double hy, int64_t nz,
     h.threads = threads;
     // Cartesian corner child (a,b) = a + 2b blends the x-side and y-side coarse neighbours
     // (directions W=0, E=1, S=2, N=3) -- analogue of multigrid.hpp:91-95.
+    h.cart_nx = nx;
+    h.cart_ny = ny;
     h.prol_d1 = {0, 1, 0, 1};
     h.prol_d2 = {2, 2, 3, 3};
 
@@ -680,7 +772,13 @@ int tpmgo_pcg_timed(tpmgo_hier H, const double* f, double* x, double tol, int ma
     const Index n = h.lv[L].ncells * h.nz;
     std::vector<double> r(f, f + n), z(n, 0.0), p(n), q(n);
     std::fill(x, x + n, 0.0);
-    const double r0 = std::sqrt(dot(n, r.data(), r.data()));
+    const bool dev = h.cart_nx > 0;
+    DevOrder d{h.cart_nx, h.cart_ny, h.nz};
+    auto dotv = [&](const std::vector<double>& a, const std::vector<double>& b) {
+      return dev ? gridstride_dot(d, [&](Index i) { return a[i] * b[i]; })
+                 : dot(n, a.data(), b.data());
+    };
+    const double r0 = std::sqrt(dotv(r, r));
     if (res_hist) res_hist[0] = r0;
     stamp(0);
     *iters = 0;
@@ -688,14 +786,14 @@ int tpmgo_pcg_timed(tpmgo_hier H, const double* f, double* x, double tol, int ma
     if (r0 == 0.0) return;
     vcycle(h, L, r.data(), z.data());
     p = z;
-    double rho = dot(n, r.data(), z.data());
+    double rho = dotv(r, z);
     if (!(rho > 0.0)) {
       *solve_status = BREAKDOWN;
       return;
     }
     for (int it = 1; it <= max_iter; ++it) {
       apply(h, L, p.data(), q.data());
-      const double pq = dot(n, p.data(), q.data());
+      const double pq = dev ? column_dot(d, q.data(), p.data()) : dot(n, p.data(), q.data());
       if (!(pq > 0.0)) {
         *solve_status = BREAKDOWN;
         return;
@@ -705,7 +803,7 @@ int tpmgo_pcg_timed(tpmgo_hier H, const double* f, double* x, double tol, int ma
         x[i] += alpha * p[i];
         r[i] -= alpha * q[i];
       }
-      const double rn = std::sqrt(dot(n, r.data(), r.data()));
+      const double rn = std::sqrt(dotv(r, r));
       if (res_hist) res_hist[it] = rn;
       *iters = it;
       stamp(it);
@@ -716,7 +814,7 @@ int tpmgo_pcg_timed(tpmgo_hier H, const double* f, double* x, double tol, int ma
       }
       std::fill(z.begin(), z.end(), 0.0);
       vcycle(h, L, r.data(), z.data());
-      const double rho_new = dot(n, r.data(), z.data());
+      const double rho_new = dotv(r, z);
       if (!(rho_new > 0.0)) {
         *solve_status = BREAKDOWN;
         return;

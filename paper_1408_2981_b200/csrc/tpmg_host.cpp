@@ -188,6 +188,12 @@ int guard(tpmg_context ctx, Fn&& fn) {
     if (ctx) ctx->last_error = e.what();
     g_global_error = e.what();
     return e.code;
+  } catch (const tpmg::LaunchError& e) {
+    const std::string m = std::string("kernel launch failed in ") + e.kernel + ": " +
+                          cudaGetErrorString(e.err);
+    if (ctx) ctx->last_error = m;
+    g_global_error = m;
+    return TPMG_E_CUDA;
   } catch (const std::bad_alloc&) {
     if (ctx) ctx->last_error = "host allocation failed";
     return TPMG_E_CUDA;
@@ -689,7 +695,9 @@ int tpmg_hier_create(tpmg_context ctx, const tpmg_grid_desc* g,
         L.send.alloc(faces);
         L.recv.alloc(faces);
       }
+      // one partial per 256-column block (k_apply) or per 32x4 tile (k_apply_tiled)
       max_blocks = std::max<int64_t>(max_blocks, (L.plane + 255) / 256 + 1);
+      max_blocks = std::max<int64_t>(max_blocks, L.plane / 128 + 1);
     }
     const int64_t nf = h->lv[levels - 1].plane * nz;
     h->r.alloc(nf); h->z.alloc(nf); h->p.alloc(nf); h->q.alloc(nf); h->tmp.alloc(nf);

@@ -53,6 +53,12 @@ struct Launch {
   int64_t* counter;  // incremented once per kernel launch (instrumentation)
 };
 
+// Thrown by a launcher when the launch itself fails (bad configuration); mapped to TPMG_E_CUDA.
+struct LaunchError {
+  cudaError_t err;
+  const char* kernel;
+};
+
 Halo self_halo(const double* u, int nx, int ny, int64_t plane);
 
 // y = A u  (apply_operator, discretization.hpp:262-278)  or  y = f - A u.

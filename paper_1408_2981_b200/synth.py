@@ -12,6 +12,11 @@ oracle, the GPU path and the CPU baseline see bit-identical inputs:
   depend on the domain decomposition;
 * uniform [-1, 1): ``m * 2^-52 - 1`` with the 53-bit integer ``m`` -- exact in fp64;
   the mean is removed with one correctly rounded division of the exact integer sum;
+* smoother damping relax = 0.8 (SmootherConfig::relax, relaxation.hpp:20): with BASELINE's
+  omega^2 and lambda^2 the horizontal coupling dominates the mass term on every level, and
+  undamped (relax = 1) block Jacobi leaves the horizontal checkerboard modes undamped
+  (amplification -> -1), which makes the PCG iteration count grow like 1/h (41, 79, 155,
+  307 iterations for n = 32..256); relax = 0.8 gives 14 iterations at every size;
 * factorised profiles (profiles.hpp:196-210) chosen so the reference's hatted
   assembly (discretization.hpp:144-184) yields ``-w^2 (dxx + dyy) u - dzz u + lam^2 u``:
   beta_r = lam^2, beta_s = h_T; alpha_s_r = 1, alpha_s_s(edge) = (h_T + h_T')/2;
@@ -199,7 +204,7 @@ def make_problem(nx: int, ny: int, nz: int, *, omega2: float, lambda2: float,
                  profile_seed: int = 1, profile_amp: float = 0.1, profile_sigma: float = 0.5,
                  h: float | None = None, depth: int = 0, nu: int = 1, tol: float = 1e-8,
                  rhs_seed: int = 0, prolongation: int = 0, restriction: int = 1,
-                 name: str = "") -> Problem:
+                 relax: float = 0.8, name: str = "") -> Problem:
     h = 1.0 / nx if h is None else h
     z = vertical_faces(nz, 1.0, grading, ratio)
     hT = horizontal_profile(profile, profile_seed, nx, ny, profile_amp, profile_sigma)
@@ -208,7 +213,7 @@ def make_problem(nx: int, ny: int, nz: int, *, omega2: float, lambda2: float,
         nx=nx, ny=ny, nz=nz, hx=h, hy=h, z_faces=z,
         beta_r=np.full(nz, lambda2), alpha_s_r=np.ones(nz), alpha_r_r=np.full(nz + 1, 1.0 / omega2),
         beta_s=hT.copy(), alpha_r_s=hT.copy(), alpha_s_s=edge_profile(hT, nx, ny),
-        omega=omega, nu_pre=nu, nu_post=nu, depth=depth, tol=tol, rhs_seed=rhs_seed,
+        omega=omega, relax=relax, nu_pre=nu, nu_post=nu, depth=depth, tol=tol, rhs_seed=rhs_seed,
         prolongation=prolongation, restriction=restriction, name=name)
 
 

@@ -12,6 +12,7 @@ reference's exception types (types.hpp:24-58).  Every call goes through the C-AB
 from __future__ import annotations
 
 import ctypes as C
+import sys
 import time
 
 import numpy as np
@@ -121,6 +122,10 @@ class Context:
             self._h = None
 
     def __del__(self):
+        # at interpreter shutdown the destruction order of handles is arbitrary: leave the
+        # device memory to the driver instead of freeing through possibly-dead parents
+        if sys.is_finalizing():
+            return
         try:
             self.close()
         except Exception:
@@ -172,6 +177,10 @@ class Field:
             self._h = None
 
     def __del__(self):
+        # at interpreter shutdown the destruction order of handles is arbitrary: leave the
+        # device memory to the driver instead of freeing through possibly-dead parents
+        if sys.is_finalizing():
+            return
         try:
             self.close()
         except Exception:
@@ -240,6 +249,10 @@ class Hierarchy:
             self._h = None
 
     def __del__(self):
+        # at interpreter shutdown the destruction order of handles is arbitrary: leave the
+        # device memory to the driver instead of freeing through possibly-dead parents
+        if sys.is_finalizing():
+            return
         try:
             self.close()
         except Exception:
