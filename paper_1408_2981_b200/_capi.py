@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_NAMES = {"fast": "libtpmg_b200.so", "strict": "libtpmg_b200_strict.so"}
+LIB_NAMES = {"exact": "libtpmg_b200.so", "fma": "libtpmg_b200_fma.so"}
 
 _D = C.POINTER(C.c_double)
 _VP = C.c_void_p
@@ -79,11 +79,11 @@ class MGConfig(C.Structure):
 _libs: dict = {}
 
 
-def lib_path(variant: str = "fast") -> str:
+def lib_path(variant: str = "exact") -> str:
     return os.path.join(PKG_DIR, LIB_NAMES[variant])
 
 
-def load(variant: str = "fast"):
+def load(variant: str = "exact"):
     """Load (once) the C-ABI library; raises if the CUDA extension was not built."""
     if variant in _libs:
         return _libs[variant]

@@ -3,8 +3,9 @@
     python -m paper_1408_2981_b200.build [--force]
 
 Produces, next to this file:
-  libtpmg_b200.so         production library (nvcc contracts a*b+c into DFMA)
-  libtpmg_b200_strict.so  same sources with --fmad=false: bitwise comparable to the oracle
+  libtpmg_b200.so       the product: the reference's exact operation order (--fmad=false,
+                        true IEEE divisions), bitwise comparable to the oracle
+  libtpmg_b200_fma.so   experimental: DFMA contraction + one reciprocal per Thomas level
 and oracle/liboracle.so (test infrastructure).
 """
 from __future__ import annotations
@@ -38,12 +39,12 @@ def _stale(target: str) -> bool:
 
 
 def build_lib(variant: str, force: bool = False, verbose: bool = False) -> str:
-    name = "libtpmg_b200.so" if variant == "fast" else "libtpmg_b200_strict.so"
+    name = "libtpmg_b200.so" if variant == "exact" else "libtpmg_b200_fma.so"
     out = os.path.join(PKG, name)
     if not force and not _stale(out):
         return out
     flags = list(COMMON)
-    if variant == "strict":
+    if variant == "exact":
         flags += ["--fmad=false", "-DTPMG_STRICT=1"]
     cmd = [_nvcc(), *ARCH, *flags, *SOURCES, "-o", out + ".tmp"]
     if verbose:
@@ -63,7 +64,7 @@ def build_oracle(force: bool = False) -> str:
 
 
 def build_all(force: bool = False, verbose: bool = False):
-    paths = [build_lib("fast", force, verbose), build_lib("strict", force, verbose), build_oracle(force)]
+    paths = [build_lib("exact", force, verbose), build_lib("fma", force, verbose), build_oracle(force)]
     return paths
 
 

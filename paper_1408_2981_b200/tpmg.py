@@ -79,7 +79,7 @@ class Context:
     """One GPU (rank) -- tpmg_init / tpmg_finalize."""
 
     def __init__(self, device: int = 0, rank: int = 0, world_size: int = 1, px: int = 1,
-                 py: int = 1, nccl_id: bytes | None = None, variant: str = "fast"):
+                 py: int = 1, nccl_id: bytes | None = None, variant: str = "exact"):
         self.lib = _capi.load(variant)
         self._idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id else None
         prm = ContextParams(device, rank, world_size, px, py,
@@ -97,7 +97,7 @@ class Context:
                                              f"{msg.decode() if msg else ''}")
 
     @staticmethod
-    def nccl_unique_id(variant: str = "fast") -> bytes:
+    def nccl_unique_id(variant: str = "exact") -> bytes:
         lib = _capi.load(variant)
         buf = C.create_string_buffer(128)
         rc = lib.tpmg_nccl_unique_id(buf)

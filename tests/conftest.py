@@ -25,16 +25,18 @@ def oracle_mod():
 
 @pytest.fixture(scope="session")
 def gpu_ctx():
+    """The product library (exact reference arithmetic)."""
     from paper_1408_2981_b200 import tpmg
 
-    return tpmg.Context(device=0, variant="fast")
+    return tpmg.Context(device=0, variant="exact")
 
 
 @pytest.fixture(scope="session")
-def gpu_ctx_strict():
+def gpu_ctx_fma():
+    """Experimental DFMA/reciprocal build (tolerance-level parity only)."""
     from paper_1408_2981_b200 import tpmg
 
-    return tpmg.Context(device=0, variant="strict")
+    return tpmg.Context(device=0, variant="fma")
 
 
 def rng_field(seed: int, n: int) -> np.ndarray:
