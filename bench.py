@@ -242,7 +242,7 @@ def main():
     for _ in range(args.steps):
         ef.upload(fnp)
         r2 = tpmg.pcg_solve(h, ef, x, P.tol, args.max_iter)
-        xnp[:] = x.download().reshape(-1)
+        x.download(out=xnp)
         e2e_iters += r2.iterations
     e3.record(stream)
     e3.synchronize()

@@ -153,7 +153,13 @@ class Field:
         self.hier.ctx._check(self.hier.lib.tpmg_field_upload(self._h, _p(a), layout))
         return self
 
-    def download(self, layout: int = X_FASTEST) -> np.ndarray:
+    def download(self, layout: int = X_FASTEST, out: np.ndarray | None = None) -> np.ndarray:
+        """Copy to the host; `out` (e.g. a pinned buffer) is filled in place when given."""
+        if out is not None:
+            if out.dtype != np.float64 or not out.flags.c_contiguous or out.size != self.size:
+                raise shape_error("download: out must be a contiguous float64 array of the field size")
+            self.hier.ctx._check(self.hier.lib.tpmg_field_download(self._h, _p(out.reshape(-1)), layout))
+            return out
         out = np.empty(self.size, dtype=np.float64)
         self.hier.ctx._check(self.hier.lib.tpmg_field_download(self._h, _p(out), layout))
         return out.reshape(self.nz, self.ny, self.nx) if layout == X_FASTEST else out

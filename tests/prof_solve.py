@@ -1,0 +1,25 @@
+"""Profiling driver: BASELINE config 3 PCG solves through the public API (one warm-up solve,
+then TPMG_SOLVES timed solves).  Run under `ncu --metrics gpu__time_duration.sum` on the GPU
+box for the per-launch list.  Not a pytest file."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_1408_2981_b200 import synth, tpmg  # noqa: E402
+
+
+def main():
+    P = synth.baseline_config(int(os.environ.get("TPMG_CFG", "3")))
+    ctx = tpmg.Context()
+    h = tpmg.Hierarchy(ctx, P)
+    h.set_use_graphs(os.environ.get("TPMG_GRAPHS", "1") == "1")
+    f = h.field().upload(P.rhs())
+    x = h.field()
+    for i in range(1 + int(os.environ.get("TPMG_SOLVES", "1"))):
+        res = tpmg.pcg_solve(h, f, x, P.tol, 200)
+        print(f"solve {i}: {res.iterations} iterations, {res.seconds * 1e3:.1f} ms wall", flush=True)
+
+
+if __name__ == "__main__":
+    main()
