@@ -125,6 +125,16 @@ const char* tpmg_last_error(tpmg_context ctx);
 /* The cudaStream_t every call of this context is ordered on (for external CUDA-event timing). */
 int tpmg_context_stream(tpmg_context ctx, void** stream);
 
+/* ---- decomposition (pure host logic, no device needed) ------------------------------------ */
+/* 2D horizontal block decomposition used by tpmg_hier_create: full columns per rank, tiles
+ * aligned so the 2x2 children of every coarse cell stay on one rank.
+ * Fills n_levels and, per level l (0 = coarsest, up to max_levels entries each):
+ * local tile nx[l], ny[l], global offset x0[l], y0[l]; neighbour ranks nbr[0..3] = W,E,S,N
+ * (a rank is its own neighbour along a dimension with one rank: periodic self wrap). */
+int tpmg_plan_decomposition(int64_t nx, int64_t ny, int px, int py, int rank, int depth,
+                            int max_levels, int* n_levels, int64_t* tile_nx, int64_t* tile_ny,
+                            int64_t* x0, int64_t* y0, int* nbr);
+
 /* ---- hierarchy: build_hierarchy_coefficients (multigrid.hpp:242-272) ---------------------- */
 /* assemble_hatted (discretization.hpp:144-184) on every level after
  * restrict_profiles (multigrid.hpp:158-201); uploads the result, immutable. */

@@ -445,6 +445,10 @@ int tpmgo_cart_create(int64_t nx, int64_t ny, double hx, double hy, int64_t nz,
         }
         levels = depth;
       }
+      // same rule as the product (tpmg_host.cpp plan_levels): with < 3 coarse cells per
+      // dimension the W/E (S/N) neighbours coincide and the transpose stencil double counts
+      if ((prolongation == 0 || restriction == 1) && levels > 1 && (a < 3 || b < 3))
+        throw Error(E_CONFIG, "linear transfers need >= 3 coarse cells per dimension");
     }
     const Index ncf = nx * ny;
     check_finite(z, nz + 1, "z_faces");

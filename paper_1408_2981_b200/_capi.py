@@ -24,6 +24,9 @@ SIGNATURES = {
     "tpmg_finalize": (C.c_int, [_VP]),
     "tpmg_last_error": (C.c_char_p, [_VP]),
     "tpmg_context_stream": (C.c_int, [_VP, C.POINTER(C.c_void_p)]),
+    "tpmg_plan_decomposition": (C.c_int, [C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int,
+                                          C.c_int, C.POINTER(C.c_int)] + [C.POINTER(C.c_int64)] * 4
+                                + [C.POINTER(C.c_int)]),
     "tpmg_hier_create": (C.c_int, [_VP, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p, C.POINTER(_VP)]),
     "tpmg_hier_destroy": (C.c_int, [_VP]),
     "tpmg_hier_n_levels": (C.c_int, [_VP, C.POINTER(C.c_int)]),

@@ -211,6 +211,30 @@ void check_finite(const double* p, size_t n, const char* what) {
       throw Error(TPMG_E_NONFINITE, std::string("non-finite values in ") + what);
 }
 
+// Number of levels of the horizontal hierarchy: tiles must stay even so the 2x2 children of
+// a coarse cell share a rank; depth 0 coarsens while the global grid stays >= 4 per dimension.
+int plan_levels(int64_t NX, int64_t NY, int px, int py, int depth, bool linear) {
+  if (NX < 1 || NY < 1 || px < 1 || py < 1) throw Error(TPMG_E_CONFIG, "bad decomposition");
+  if (NX % px || NY % py)
+    throw Error(TPMG_E_CONFIG, "global grid does not split evenly over the process grid");
+  int levels = 1;
+  int64_t a = NX / px, b = NY / py, ga = NX, gb = NY;
+  if (depth <= 0) {
+    while (a % 2 == 0 && b % 2 == 0 && ga / 2 >= 4 && gb / 2 >= 4) {
+      a /= 2; b /= 2; ga /= 2; gb /= 2; ++levels;
+    }
+  } else {
+    for (int l = 1; l < depth; ++l) {
+      if (a % 2 || b % 2) throw Error(TPMG_E_CONFIG, "tile does not coarsen to the requested depth");
+      a /= 2; b /= 2; ga /= 2; gb /= 2;
+    }
+    levels = depth;
+  }
+  if (linear && levels > 1 && (ga < 3 || gb < 3))
+    throw Error(TPMG_E_CONFIG, "linear transfers need >= 3 coarse cells per dimension");
+  return levels;
+}
+
 // ---- halos -----------------------------------------------------------------------------
 // Exchange the 1-cell faces of u on level l with the 4 neighbouring ranks and return the
 // view the kernels read across the tile faces.  Dimensions with a single rank wrap onto the
@@ -526,6 +550,29 @@ int tpmg_context_stream(tpmg_context ctx, void** stream) {
   return TPMG_OK;
 }
 
+int tpmg_plan_decomposition(int64_t nx, int64_t ny, int px, int py, int rank, int depth,
+                            int max_levels, int* n_levels, int64_t* tile_nx, int64_t* tile_ny,
+                            int64_t* x0, int64_t* y0, int* nbr) {
+  return guard(nullptr, [&] {
+    if (rank < 0 || rank >= px * py) throw Error(TPMG_E_CONFIG, "rank outside the process grid");
+    const int levels = plan_levels(nx, ny, px, py, depth, false);
+    *n_levels = levels;
+    const int rx = rank % px, ry = rank / px;
+    for (int l = 0; l < levels && l < max_levels; ++l) {
+      const int64_t gx = nx >> (levels - 1 - l), gy = ny >> (levels - 1 - l);
+      tile_nx[l] = gx / px;
+      tile_ny[l] = gy / py;
+      x0[l] = rx * tile_nx[l];
+      y0[l] = ry * tile_ny[l];
+    }
+    auto rk = [&](int x, int y) { return ((y % py + py) % py) * px + ((x % px + px) % px); };
+    nbr[0] = rk(rx - 1, ry);
+    nbr[1] = rk(rx + 1, ry);
+    nbr[2] = rk(rx, ry - 1);
+    nbr[3] = rk(rx, ry + 1);
+  });
+}
+
 int tpmg_hier_create(tpmg_context ctx, const tpmg_grid_desc* g,
                      const tpmg_factorized_profiles* p, double omega, const tpmg_mg_config* cfg,
                      tpmg_hierarchy* out) {
@@ -558,26 +605,9 @@ int tpmg_hier_create(tpmg_context ctx, const tpmg_grid_desc* g,
     if (p->xi_r_s) check_finite(p->xi_r_s, ncf, "xi_r_s");
     check_finite(p->alpha_s_s, 2 * ncf, "alpha_s_s");
 
-    // levels: tiles must stay even so the 2x2 children of a coarse cell share a rank
-    int levels = 1;
-    {
-      int64_t a = NX / ctx->px, b = NY / ctx->py, ga = NX, gb = NY;
-      if (cfg->depth <= 0) {
-        while (a % 2 == 0 && b % 2 == 0 && ga / 2 >= 4 && gb / 2 >= 4) {
-          a /= 2; b /= 2; ga /= 2; gb /= 2; ++levels;
-        }
-      } else {
-        for (int l = 1; l < cfg->depth; ++l) {
-          if (a % 2 || b % 2)
-            throw Error(TPMG_E_CONFIG, "tile does not coarsen to the requested depth");
-          a /= 2; b /= 2; ga /= 2; gb /= 2;
-        }
-        levels = cfg->depth;
-      }
-      if (cfg->prolongation == TPMG_PROLONG_LINEAR || cfg->restriction == TPMG_RESTRICT_TRANSPOSE)
-        if (levels > 1 && (ga < 3 || gb < 3))
-          throw Error(TPMG_E_CONFIG, "linear transfers need >= 3 coarse cells per dimension");
-    }
+    const int levels = plan_levels(NX, NY, ctx->px, ctx->py, cfg->depth,
+                                   cfg->prolongation == TPMG_PROLONG_LINEAR ||
+                                       cfg->restriction == TPMG_RESTRICT_TRANSPOSE);
 
     auto h = std::make_unique<tpmg_hierarchy_s>();
     h->ctx = ctx;
