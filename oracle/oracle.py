@@ -86,6 +86,43 @@ class OracleHierarchy:
         _chk(rc)
         return cls(h, P.nz)
 
+    @classmethod
+    def from_tables(cls, nz, nnb, nchild, ncells, nedges, nbr, cedge, children, prol_d1, prol_d2,
+                    bv, sv, av, xv, bh, ah, xh, sh, relax, prolongation, restriction, nu_pre,
+                    nu_post, threads=1):
+        """Generic tables (tpmgo_generic_create), e.g. the reference's icosahedral hierarchy."""
+        nl = len(ncells)
+        I64P = C.POINTER(C.c_int64)
+        keep = []
+
+        def i64(a):
+            a = np.ascontiguousarray(a, dtype=np.int64)
+            keep.append(a)
+            return a.ctypes.data_as(I64P)
+
+        def f64(a):
+            a = np.ascontiguousarray(a, dtype=np.float64)
+            keep.append(a)
+            return a.ctypes.data_as(_D)
+
+        nbr_p = (I64P * nl)(*[i64(a) for a in nbr])
+        ced_p = (I64P * nl)(*[i64(a) for a in cedge])
+        ch_p = (I64P * nl)(*[i64(a) if a is not None else None for a in children])
+        bh_p = (_D * nl)(*[f64(a) for a in bh])
+        ah_p = (_D * nl)(*[f64(a) for a in ah])
+        xh_p = (_D * nl)(*[f64(a) for a in xh])
+        sh_p = (_D * nl)(*[f64(a) for a in sh])
+        d1 = (C.c_int * nchild)(*prol_d1)
+        d2 = (C.c_int * nchild)(*prol_d2)
+        h = C.c_void_p()
+        rc = lib().tpmgo_generic_create(
+            C.c_int(nl), _I64(nz), C.c_int(nnb), C.c_int(nchild), i64(ncells), i64(nedges),
+            nbr_p, ced_p, ch_p, d1, d2, f64(bv), f64(sv), f64(av), f64(xv), bh_p, ah_p, xh_p,
+            sh_p, C.c_double(relax), C.c_int(prolongation), C.c_int(restriction),
+            C.c_int(nu_pre), C.c_int(nu_post), C.c_int(threads), C.byref(h))
+        _chk(rc)
+        return cls(h, nz)
+
     def __del__(self):
         if getattr(self, "_h", None) is not None and _lib is not None:
             _lib.tpmgo_destroy(self._h)
