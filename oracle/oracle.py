@@ -77,10 +77,14 @@ class OracleHierarchy:
         f = lambda a: _p(np.ascontiguousarray(a, dtype=np.float64))
         keep = [np.ascontiguousarray(a, dtype=np.float64) for a in
                 (P.z_faces, P.beta_r, P.alpha_s_r, P.alpha_r_r, P.beta_s, P.alpha_r_s, P.alpha_s_s)]
+        xr = xs = None
+        if getattr(P, "xi_r_r", None) is not None:
+            xr = np.ascontiguousarray(P.xi_r_r, dtype=np.float64)
+            xs = np.ascontiguousarray(P.xi_r_s, dtype=np.float64)
         rc = lib().tpmgo_cart_create(
             _I64(P.nx), _I64(P.ny), C.c_double(P.hx), C.c_double(P.hy), _I64(P.nz),
-            _p(keep[0]), _p(keep[1]), _p(keep[2]), _p(keep[3]), None, _p(keep[4]), _p(keep[5]),
-            None, _p(keep[6]), C.c_double(P.omega), C.c_double(kw["relax"]),
+            _p(keep[0]), _p(keep[1]), _p(keep[2]), _p(keep[3]), _p(xr), _p(keep[4]), _p(keep[5]),
+            _p(xs), _p(keep[6]), C.c_double(P.omega), C.c_double(kw["relax"]),
             C.c_int(kw["prolongation"]), C.c_int(kw["restriction"]), C.c_int(kw["nu_pre"]),
             C.c_int(kw["nu_post"]), C.c_int(kw["depth"]), C.c_int(threads), C.byref(h))
         _chk(rc)

@@ -176,6 +176,8 @@ class Problem:
     tol: float = 1e-8
     rhs_seed: int = 0
     name: str = ""
+    xi_r_r: np.ndarray | None = None  # vertical advection (nz+1), None = xi == 0
+    xi_r_s: np.ndarray | None = None  # (nx*ny)
 
     @property
     def n_dof(self) -> int:

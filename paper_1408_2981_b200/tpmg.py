@@ -206,7 +206,12 @@ class Hierarchy:
                        P.alpha_s_s)]
         z, br, asr, arr, bs, ars, ass = self._keep
         grid = GridDesc(P.nx, P.ny, P.hx, P.hy, P.nz, _p(z))
-        prof = FactorizedProfiles(_p(br), _p(asr), _p(arr), None, _p(bs), _p(ars), None, _p(ass))
+        xr = xs = None
+        if getattr(P, "xi_r_r", None) is not None:
+            xr = np.ascontiguousarray(P.xi_r_r, dtype=np.float64)
+            xs = np.ascontiguousarray(P.xi_r_s, dtype=np.float64)
+            self._keep += [xr, xs]
+        prof = FactorizedProfiles(_p(br), _p(asr), _p(arr), _p(xr), _p(bs), _p(ars), _p(xs), _p(ass))
         cfg = MGConfig(kw.get("smoother", 0), kw["relax"], kw["prolongation"], kw["restriction"],
                        kw["nu_pre"], kw["nu_post"], kw["depth"])
         h = C.c_void_p()
