@@ -65,6 +65,26 @@ def test_init_fails_loudly_without_device():
         tpmg.Context()
 
 
+def test_cpp_adapter_builds_and_links(tmp_path):
+    """include/tpmg_b200.hpp (reference-shaped C++ calls) compiles and links against the
+    C-ABI library; without a device the Context constructor throws (no CPU fallback)."""
+    import torch
+
+    src = tmp_path / "use.cpp"
+    src.write_text(
+        '#include "tpmg_b200.hpp"\n#include <cstdio>\n'
+        "int main() {\n"
+        "  try { tpmg_b200::Context ctx(0); std::puts(\"device\"); return 0; }\n"
+        "  catch (const tpmg_b200::device_error& e) { std::puts(\"no device\"); return 3; }\n"
+        "}\n")
+    exe = tmp_path / "use"
+    pkg = os.path.dirname(_capi.lib_path("exact"))
+    subprocess.run(["g++", "-std=c++17", "-I", os.path.join(ROOT, "include"), str(src), "-o",
+                    str(exe), "-L", pkg, "-l:libtpmg_b200.so", f"-Wl,-rpath,{pkg}"], check=True)
+    rc = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert rc.returncode == (0 if torch.cuda.is_available() else 3), rc.stdout + rc.stderr
+
+
 def plan(nx, ny, px, py, rank, depth=0):
     L = _capi.load("exact")
     n = C.c_int()
