@@ -74,6 +74,7 @@ struct Hier {
   std::vector<int> nu_pre, nu_post;
   int threads = 1;
   Index cart_nx = 0, cart_ny = 0;  // finest Cartesian dims (0 for generic tables)
+  int pcg_fused = -1;              // -1: device rule, 0/1: forced
 };
 
 // ColumnMatrix, discretization.hpp:208-231.
@@ -350,12 +351,16 @@ double gridstride_dot(const DevOrder& d, Val val) {
 }
 
 // fused p.q of the apply kernel: per-column sums over k, then per-CTA trees.
-double column_dot(const DevOrder& d, const double* y, const double* u) {
+// descending: the per-column sum runs k = nz-1 .. 0 (sums formed in a back substitution)
+double column_dot(const DevOrder& d, const double* y, const double* u, bool descending = false) {
   const Index plane = d.plane();
   std::vector<double> colsum(plane);
   for (Index c = 0; c < plane; ++c) {
     double a = 0.0;
-    for (Index k = 0; k < d.nz; ++k) a += y[c * d.nz + k] * u[c * d.nz + k];
+    if (descending)
+      for (Index k = d.nz - 1; k >= 0; --k) a += y[c * d.nz + k] * u[c * d.nz + k];
+    else
+      for (Index k = 0; k < d.nz; ++k) a += y[c * d.nz + k] * u[c * d.nz + k];
     colsum[c] = a;
   }
   std::vector<double> part;
@@ -629,6 +634,11 @@ void tpmgo_destroy(tpmgo_hier h) { delete h; }
 int tpmgo_n_levels(tpmgo_hier h) { return static_cast<int>(h->h.lv.size()); }
 int64_t tpmgo_n_cells(tpmgo_hier h, int level) { return h->h.lv[level].ncells; }
 int64_t tpmgo_nz(tpmgo_hier h) { return h->h.nz; }
+int tpmgo_set_pcg_fused(tpmgo_hier h, int mode) {
+  h->h.pcg_fused = mode;
+  return OK;
+}
+
 int tpmgo_set_threads(tpmgo_hier h, int threads) {
   h->h.threads = threads;
   return OK;
@@ -782,6 +792,16 @@ int tpmgo_pcg_timed(tpmgo_hier H, const double* f, double* x, double tol, int ma
       return dev ? gridstride_dot(d, [&](Index i) { return a[i] * b[i]; })
                  : dot(n, a.data(), b.data());
     };
+    // The device fuses |r|^2 into the first and r.z into the last finest-level sweep when the
+    // finest level runs the tiled TMEM smoother (tpmg_host.cpp pcg_iteration); those partials
+    // are per-column sums reduced per 32x4 tile.
+    int cols = 32;
+    while (cols < 2 * h.nz) cols <<= 1;
+    const int Lf = static_cast<int>(h.lv.size()) - 1;
+    const bool fused = dev && (h.pcg_fused >= 0 ? h.pcg_fused == 1
+                                                : (h.cart_nx % 32 == 0 && h.cart_ny % 4 == 0 &&
+                                                   h.nz % 4 == 0 && cols <= 512 && Lf > 0 &&
+                                                   h.nu_pre[Lf] >= 1 && h.nu_post[Lf] >= 1));
     const double r0 = std::sqrt(dotv(r, r));
     if (res_hist) res_hist[0] = r0;
     stamp(0);
@@ -807,7 +827,7 @@ int tpmgo_pcg_timed(tpmgo_hier H, const double* f, double* x, double tol, int ma
         x[i] += alpha * p[i];
         r[i] -= alpha * q[i];
       }
-      const double rn = std::sqrt(dotv(r, r));
+      const double rn = std::sqrt(fused ? column_dot(d, r.data(), r.data()) : dotv(r, r));
       if (res_hist) res_hist[it] = rn;
       *iters = it;
       stamp(it);
@@ -818,7 +838,7 @@ int tpmgo_pcg_timed(tpmgo_hier H, const double* f, double* x, double tol, int ma
       }
       std::fill(z.begin(), z.end(), 0.0);
       vcycle(h, L, r.data(), z.data());
-      const double rho_new = dotv(r, z);
+      const double rho_new = fused ? column_dot(d, r.data(), z.data(), true) : dotv(r, z);
       if (!(rho_new > 0.0)) {
         *solve_status = BREAKDOWN;
         return;

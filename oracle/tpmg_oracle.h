@@ -68,6 +68,8 @@ int tpmgo_n_levels(tpmgo_hier h);
 int64_t tpmgo_n_cells(tpmgo_hier h, int level);
 int64_t tpmgo_nz(tpmgo_hier h);
 int tpmgo_set_threads(tpmgo_hier h, int threads);
+/* Reduction order of the PCG dots: -1 = the device's rule (default), 0 = plain, 1 = fused. */
+int tpmgo_set_pcg_fused(tpmgo_hier h, int mode);
 
 /* Hatted coefficients of a level (assemble_hatted, discretization.hpp:144-184). */
 int tpmgo_get_coefficients(tpmgo_hier h, int level, double* bh, double* ah, double* xh,

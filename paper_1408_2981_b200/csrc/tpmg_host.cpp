@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -160,6 +161,7 @@ struct tpmg_hierarchy_s {
   int* d_err = nullptr;
   double* h_scal = nullptr;  // pinned
   bool use_graphs = true;
+  bool pcg_fused = false;  // PCG vector work fused into the finest-level smoother sweeps
   std::unordered_map<const double*, cudaGraphExec_t> iter_graphs;
   std::unordered_map<const double*, int64_t> iter_graph_kernels;
   int finest() const { return (int)lv.size() - 1; }
@@ -308,11 +310,16 @@ void apply_level(tpmg_hierarchy h, int l, int mode, const double* u, const doubl
   if (dot_slot >= 0) finish_dot(h, nb, dot_slot);
 }
 
-void sweep(tpmg_hierarchy h, int l, const double* u_in, const double* f, double* out) {
+// One line-Jacobi sweep.  With `fz` the sweep also does fused PCG work (see PcgFuse) and its
+// per-tile partials are reduced into scalar slot `slot`.
+void sweep(tpmg_hierarchy h, int l, const double* u_in, const double* f, double* out,
+           const tpmg::PcgFuse* fz = nullptr, int slot = -1) {
   Level& L = h->lv[l];
   Halo H = u_in ? exchange(h, l, u_in) : tpmg::self_halo(out, L.nx, L.ny, L.plane);
+  int nb = 0;
   tpmg::launch_jacobi(h->ctx->launch(), h->vcoef(), L.coef(h->nz), h->xi, u_in, H, f, out,
-                      h->relax, h->d_err);
+                      h->relax, h->d_err, fz, &nb);
+  if (fz) finish_dot(h, nb, slot);
 }
 
 // fine level lf -> coarse lf-1: coarse = R (f - A u).  `scratch` is a free fine-level buffer.
@@ -355,18 +362,29 @@ void fill(tpmg_hierarchy h, double* p, int64_t n, double v) {
 
 // v_cycle, multigrid.hpp:276-299.  On return the iterate is in A; B is scratch of the same
 // level.  zero: A's content is ignored and treated as 0 (the preconditioner / coarse case).
-void vcycle(tpmg_hierarchy h, int l, const double* f, double* A, double* B, bool zero) {
+//
+// pcg_fuse (finest level of a fused PCG iteration, f == r): the first sweep from zero also does
+// r -= alpha q and |r|^2 (slot 2); the last post-sweep also does r.z (slot 3).
+void vcycle(tpmg_hierarchy h, int l, const double* f, double* A, double* B, bool zero,
+            bool pcg_fuse = false) {
   Level& L = h->lv[l];
   const int64_t n = L.plane * h->nz;
   const int npre = h->nu_pre[l], npost = h->nu_post[l], total = npre + npost;
   double* cur = A;
   auto other = [&](double* c) { return c == A ? B : A; };
   int s0 = 0;
+  tpmg::PcgFuse fz;
+  if (pcg_fuse) {
+    fz.q = h->q.p;
+    fz.r = h->r.p;
+    fz.s = h->scal.p;
+    fz.partials = h->partials.p;
+  }
   if (zero) {
     if (npre > 0) {
       // first sweep from zero writes where the last sweep must end in A
       cur = ((total - 1) % 2 == 0) ? A : B;
-      sweep(h, l, nullptr, f, cur);
+      sweep(h, l, nullptr, f, cur, pcg_fuse ? &fz : nullptr, 2);
       s0 = 1;
     } else {
       cur = (npost % 2 == 0) ? A : B;
@@ -386,7 +404,8 @@ void vcycle(tpmg_hierarchy h, int l, const double* f, double* A, double* B, bool
   }
   for (int s = 0; s < npost; ++s) {
     double* out = other(cur);
-    sweep(h, l, cur, f, out);
+    const bool last = pcg_fuse && s + 1 == npost;
+    sweep(h, l, cur, f, out, last ? &fz : nullptr, 3);
     cur = out;
   }
   if (cur != A)
@@ -420,12 +439,27 @@ void same_hier(tpmg_hierarchy h, tpmg_field f) {
   if (field_of(f)->h != h) throw Error(TPMG_E_SHAPE, "field belongs to another hierarchy");
 }
 
-// PCG iteration body (no host synchronisation): q = A p, p.q; x += a p, r -= a q, r.r;
-// z = V(r); r.z; p = z + b p.   Scalars: s[0]=rho, s[1]=p.q, s[2]=r.r, s[3]=rho_new.
-void pcg_iteration(tpmg_hierarchy h, double* x) {
+// PCG iteration body (no host synchronisation).  Scalars: s[0]=rho, s[1]=p.q, s[2]=r.r,
+// s[3]=rho_new.
+// Fused schedule (h->pcg_fused): [x += a_prev p_old; p = z + b p_old; rho <- rho_new] (skipped
+// on the first iteration, where p = z, x = 0); q = A p with p.q; V-cycle whose first finest
+// sweep does r -= a q and r.r, and whose last finest sweep forms r.z.  The x update of the
+// final iteration is applied after the loop (k_pcg_xfinal).  Every element is computed with
+// the same operations as the plain schedule: q = A p, p.q; x += a p, r -= a q, r.r;
+// z = V(r); r.z; p = z + b p.
+void pcg_iteration(tpmg_hierarchy h, double* x, bool first = false) {
   const int L = h->finest();
   const int64_t n = h->lv[L].plane * h->nz;
   tpmg_context ctx = h->ctx;
+  if (h->pcg_fused) {
+    if (!first) {
+      tpmg::launch_pcg_px(ctx->launch(), n, h->scal.p, h->z.p, h->p.p, x);
+      tpmg::launch_copy_scalar(ctx->launch(), h->scal.p, 0, 3);
+    }
+    apply_level(h, L, tpmg::APPLY_AU, h->p.p, nullptr, h->q.p, 1);
+    vcycle(h, L, h->r.p, h->z.p, h->tmp.p, true, true);
+    return;
+  }
   apply_level(h, L, tpmg::APPLY_AU, h->p.p, nullptr, h->q.p, 1);
   int nb = 0;
   tpmg::launch_pcg_xr(ctx->launch(), n, h->scal.p, x, h->r.p, h->p.p, h->q.p, h->partials.p, &nb);
@@ -436,10 +470,10 @@ void pcg_iteration(tpmg_hierarchy h, double* x) {
   tpmg::launch_copy_scalar(ctx->launch(), h->scal.p, 0, 3);
 }
 
-void run_iteration(tpmg_hierarchy h, double* x) {
+void run_iteration(tpmg_hierarchy h, double* x, bool first) {
   tpmg_context ctx = h->ctx;
-  if (!h->use_graphs) {
-    pcg_iteration(h, x);
+  if (!h->use_graphs || (first && h->pcg_fused)) {
+    pcg_iteration(h, x, first);
     return;
   }
   auto it = h->iter_graphs.find(x);
@@ -737,6 +771,13 @@ int tpmg_hier_create(tpmg_context ctx, const tpmg_grid_desc* g,
     CUDA_CHECK(cudaMalloc(&h->d_err, sizeof(int)));
     CUDA_CHECK(cudaMemset(h->d_err, 0, sizeof(int)));
     CUDA_CHECK(cudaMallocHost(&h->h_scal, 8 * sizeof(double)));
+    {
+      const int L = levels - 1;
+      const char* e = getenv("TPMG_PCG_FUSED");
+      const bool allow = !(e && atoi(e) == 0);
+      h->pcg_fused = allow && L > 0 && h->nu_pre[L] >= 1 && h->nu_post[L] >= 1 &&
+                     tpmg::jacobi_fusable(h->lv[L].coef(h->nz));
+    }
     *out = h.release();
   });
 }
@@ -1017,8 +1058,15 @@ int tpmg_pcg(tpmg_hierarchy h, tpmg_field f, tpmg_field x, double tol, int max_i
       *solve_status = TPMG_BREAKDOWN;
       return;
     }
+    // fused schedule: the last iteration's x += alpha p is still pending when the loop ends
+    auto finish_x = [&] {
+      if (h->pcg_fused) {
+        tpmg::launch_pcg_xfinal(ctx->launch(), n, h->scal.p, h->p.p, x->buf.p);
+        sync_check(h);
+      }
+    };
     for (int it = 1; it <= max_iter; ++it) {
-      run_iteration(h, x->buf.p);
+      run_iteration(h, x->buf.p, it == 1);
       CUDA_CHECK(cudaMemcpyAsync(h->h_scal, h->scal.p, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
       sync_check(h);
       const double pq = h->h_scal[1], rr = h->h_scal[2], rho_new = h->h_scal[3];
@@ -1029,17 +1077,23 @@ int tpmg_pcg(tpmg_hierarchy h, tpmg_field f, tpmg_field x, double tol, int max_i
       const double rn = std::sqrt(rr);
       if (res_hist) res_hist[it] = rn;
       *iters = it;
-      if (rn / r0 <= tol) return;
+      if (rn / r0 <= tol) {
+        finish_x();
+        return;
+      }
       if (rn / r0 > 1e4) {
         *solve_status = TPMG_DIVERGED;
+        finish_x();
         return;
       }
       if (!(rho_new > 0.0)) {
         *solve_status = TPMG_BREAKDOWN;
+        finish_x();
         return;
       }
     }
     *solve_status = TPMG_NOT_CONVERGED;
+    finish_x();
   });
 }
 

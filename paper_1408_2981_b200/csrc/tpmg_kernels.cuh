@@ -68,11 +68,29 @@ void launch_apply(const Launch& L, const VertCoef& V, const LevelCoef& C, bool x
                   const double* u, const Halo& H, const double* f, double* y,
                   double* dot_partials, int* nblocks);
 
+// PCG work fused into the finest-level line smoother (tiled TMEM path only).  Zero-guess
+// sweep: f (== r) is replaced in place by r - alpha q (alpha = s[0]/s[1]) and per-tile |r|^2
+// partials are written; nonzero-guess sweep: per-tile partials of f.out (r.z).
+struct PcgFuse {
+  const double* q = nullptr;
+  double* r = nullptr;
+  const double* s = nullptr;
+  double* partials = nullptr;
+};
+
 // One block-Jacobi line sweep (smooth, relaxation.hpp:77-97): out = u + relax * T^{-1}(f - A u);
 // u == nullptr means a zero initial guess.  Zero pivots set bit 1 in *err.
 void launch_jacobi(const Launch& L, const VertCoef& V, const LevelCoef& C, bool xi,
                    const double* u, const Halo& H, const double* f, double* out, double relax,
-                   int* err);
+                   int* err, const PcgFuse* fuse = nullptr, int* nblocks = nullptr);
+// True when launch_jacobi takes the tiled TMEM path on this level (the fused PCG modes).
+bool jacobi_fusable(const LevelCoef& C);
+
+// x += alpha p_old; p = z + beta p_old   (alpha = s[0]/s[1], beta = s[3]/s[0])
+void launch_pcg_px(const Launch& L, int64_t n, const double* s, const double* z, double* p,
+                   double* x);
+// x += alpha p   (alpha = s[0]/s[1])
+void launch_pcg_xfinal(const Launch& L, int64_t n, const double* s, const double* p, double* x);
 
 // coarse = R_sum(fine) (restrict_field, multigrid.hpp:29-43).
 void launch_restrict_sum(const Launch& L, int cnx, int cny, int nz, const double* fine,
