@@ -373,13 +373,13 @@ double column_dot(const DevOrder& d, const double* y, const double* u, bool desc
         for (int t = 0; t < 128; ++t) acc[t] = colsum[(by * 4 + t / 32) * d.nx + bx * 32 + t % 32];
         part[by * gx + bx] = block_tree(acc, 128);
       }
-  } else {  // k_apply: 256 consecutive columns per block
-    const Index B = (plane + 255) / 256;
+  } else {  // k_apply_small: 64 consecutive columns per block
+    const Index B = (plane + 63) / 64;
     part.resize(B);
-    double acc[256];
+    double acc[64];
     for (Index b = 0; b < B; ++b) {
-      for (int t = 0; t < 256; ++t) acc[t] = b * 256 + t < plane ? colsum[b * 256 + t] : 0.0;
-      part[b] = block_tree(acc, 256);
+      for (int t = 0; t < 64; ++t) acc[t] = b * 64 + t < plane ? colsum[b * 64 + t] : 0.0;
+      part[b] = block_tree(acc, 64);
     }
   }
   return reduce_partials(part);
