@@ -162,6 +162,7 @@ struct tpmg_hierarchy_s {
   double* h_scal = nullptr;  // pinned
   bool use_graphs = true;
   bool pcg_fused = false;  // PCG vector work fused into the finest-level smoother sweeps
+  bool fuse_rr = false;    // fused residual + transpose restriction (TPMG_FUSE_RR=1 enables)
   std::unordered_map<const double*, cudaGraphExec_t> iter_graphs;
   std::unordered_map<const double*, int64_t> iter_graph_kernels;
   int finest() const { return (int)lv.size() - 1; }
@@ -331,6 +332,9 @@ void resid_restrict(tpmg_hierarchy h, int lf, const double* u, const double* f, 
     const Halo H = exchange(h, lf, u);
     tpmg::launch_resid_restrict_sum(h->ctx->launch(), h->vcoef(), F.coef(h->nz), h->xi, u, H, f,
                                     coarse);
+  } else if (h->ctx->world == 1 && h->fuse_rr && tpmg::resid_restrict_T_fusable(F.coef(h->nz))) {
+    tpmg::launch_resid_restrict_T(h->ctx->launch(), h->vcoef(), F.coef(h->nz), h->xi, u, f,
+                                  coarse);
   } else {
     apply_level(h, lf, tpmg::APPLY_RESID, u, f, scratch);
     const Halo Hr = exchange(h, lf, scratch);
@@ -777,6 +781,9 @@ int tpmg_hier_create(tpmg_context ctx, const tpmg_grid_desc* g,
       const bool allow = !(e && atoi(e) == 0);
       h->pcg_fused = allow && L > 0 && h->nu_pre[L] >= 1 && h->nu_post[L] >= 1 &&
                      tpmg::jacobi_fusable(h->lv[L].coef(h->nz));
+      // opt-in: bitwise identical but measured slower (1.14 vs 0.80 ms at config 3)
+      const char* e2 = getenv("TPMG_FUSE_RR");
+      h->fuse_rr = e2 && atoi(e2) == 1;
     }
     *out = h.release();
   });

@@ -98,6 +98,10 @@ void launch_restrict_sum(const Launch& L, int cnx, int cny, int nz, const double
 // coarse = R_sum(f - A u) fused (multigrid.hpp:285-291), u on the fine level.
 void launch_resid_restrict_sum(const Launch& L, const VertCoef& V, const LevelCoef& Cf, bool xi,
                                const double* u, const Halo& H, const double* f, double* coarse);
+// coarse = P^T (f - A u) fused, single GPU (periodic wrap, 2-cell u halo inside the kernel).
+bool resid_restrict_T_fusable(const LevelCoef& Cf);
+void launch_resid_restrict_T(const Launch& L, const VertCoef& V, const LevelCoef& Cf, bool xi,
+                             const double* u, const double* f, double* coarse);
 // coarse = P^T fine (restrict_field_transpose, multigrid.hpp:46-69); Hf: fine face halo.
 void launch_restrict_transpose(const Launch& L, int cnx, int cny, int nz, const double* fine,
                                const Halo& Hf, double* coarse);
