@@ -47,28 +47,40 @@ class ClockSampler:
               "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, device: int):
-        self.device, self.samples, self._stop = device, [], threading.Event()
+        self.device, self.samples, self._proc = device, [], None
         self._t = threading.Thread(target=self._run, daemon=True)
+        self._active = False
 
     def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        try:
+            for line in self._proc.stdout:
+                if self._active and line.strip():
+                    self.samples.append([x.strip() for x in line.split(",")])
+        except Exception:
+            pass
 
     def __enter__(self):
-        self._t.start()
+        try:  # one streaming process (every 50 ms) instead of one process per sample
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self._t.start()
+            time.sleep(0.15)
+        except Exception:
+            self._proc = None
+        self._active = True
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        self._active = False
+        if self._proc is not None:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=5)
+            except Exception:
+                self._proc.kill()
+            self._t.join(timeout=5)
 
     def summary(self):
         if not self.samples:
@@ -107,19 +119,27 @@ def make_problem(px: int, py: int):
         nu=1, tol=1e-8, h=1.0 / 1024, name=f"cfg4_weak_{px}x{py}")
 
 
-def cpu_port_sample(P, threads: int, iters: int = 2):
-    """Oracle port timed on the host cores: seconds per PCG iteration (from the solve's
-    ConvergenceHistory seconds column) on the same problem, `iters` iterations."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle as O
-    from paper_1408_2981_b200 import synth
+class CpuPort:
+    """The oracle port (the reference's algorithm, parallel_for threading) on the host cores:
+    seconds per PCG iteration from the solve's ConvergenceHistory seconds column."""
 
-    O.build()
-    o = O.OracleHierarchy.from_problem(P, threads=threads)
-    f = synth.x_fastest_to_k_fastest(P.rhs())
-    _, hist, it, st, secs = o.pcg(f, P.tol, iters, seconds=True)
-    per_iter = (secs[it] - secs[1]) / max(it - 1, 1) if it >= 2 else secs[it]
-    return per_iter, it
+    def __init__(self, P, threads: int):
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as O
+        from paper_1408_2981_b200 import synth
+
+        O.build()
+        self.P = P
+        self.o = O.OracleHierarchy.from_problem(P, threads=threads)
+        self.f = synth.x_fastest_to_k_fastest(P.rhs())
+
+    def sample(self, iters: int = 2):
+        _, hist, it, st, secs = self.o.pcg(self.f, self.P.tol, iters, seconds=True)
+        return (secs[it] - secs[1]) / max(it - 1, 1) if it >= 2 else secs[it]
+
+
+def cpu_port_sample(P, threads: int, iters: int = 2):
+    return CpuPort(P, threads).sample(iters), iters
 
 
 def run_reference(args):
@@ -130,9 +150,10 @@ def run_reference(args):
         return 0
     P = make_problem(*proc_grid(world))
     threads = os.cpu_count() or 1
+    port = CpuPort(P, threads)
     per = []
     for s in range(args.warmup + args.steps):
-        t, it = cpu_port_sample(P, threads, iters=2)
+        t = port.sample(iters=2)
         if s >= args.warmup:
             per.append(t)
     t_iter = statistics.median(per)
@@ -155,7 +176,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
