@@ -206,7 +206,14 @@ def main():
     ctx = tpmg.Context(device=local, rank=rank, world_size=world, px=px, py=py, nccl_id=nccl_id)
     h = tpmg.Hierarchy(ctx, P)
     lnx, lny, nz, x0, y0 = h.level_shape(h.finest)
-    f_host = synth.rhs_x_fastest(P.rhs_seed, P.nx, P.ny, P.nz, x0, y0, lnx, lny)
+    if world == 1:
+        f_host = synth.rhs_x_fastest(P.rhs_seed, P.nx, P.ny, P.nz, x0, y0, lnx, lny)
+    else:  # each rank sums its own tile exactly; the integer sums are all-gathered
+        part = synth.tile_m_sum(P.rhs_seed, P.nx, P.ny, P.nz, x0, y0, lnx, lny)
+        sums = [None] * world
+        dist.all_gather_object(sums, part)
+        mean = synth.mean_from_m_sum(sum(sums), P.n_dof)
+        f_host = synth.rhs_x_fastest(P.rhs_seed, P.nx, P.ny, P.nz, x0, y0, lnx, lny, mean=mean)
     f = h.field().upload(f_host)
     x = h.field()
     stream = torch.cuda.ExternalStream(ctx.stream_handle(), device=local)

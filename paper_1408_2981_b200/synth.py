@@ -70,19 +70,40 @@ def rhs_mean(seed: int, n: int) -> float:
     return float(Fraction(s - n * (1 << 52), n * (1 << 52)))
 
 
+def tile_m_sum(seed: int, nx: int, ny: int, nz: int, x0: int, y0: int, lnx: int, lny: int) -> int:
+    """Exact integer sum of the mantissa integers m over one tile (all levels)."""
+    total = 0
+    xs = np.arange(x0, x0 + lnx, dtype=np.uint64)
+    ys = np.arange(y0, y0 + lny, dtype=np.uint64)
+    for k in range(nz):
+        idx = (np.uint64(k) * np.uint64(ny) + ys)[:, None] * np.uint64(nx) + xs[None, :]
+        m = splitmix64(seed, idx) >> np.uint64(11)
+        total += (int((m >> np.uint64(26)).sum(dtype=np.uint64)) << 26) + \
+            int((m & np.uint64((1 << 26) - 1)).sum(dtype=np.uint64))
+    return total
+
+
+def mean_from_m_sum(s: int, n: int) -> float:
+    """Correctly rounded mean of n uniform values whose mantissa integers sum to s."""
+    return float(Fraction(s - n * (1 << 52), n * (1 << 52)))
+
+
 def rhs_x_fastest(seed: int, nx: int, ny: int, nz: int, x0: int = 0, y0: int = 0,
                   lnx: int | None = None, lny: int | None = None,
-                  gnx: int | None = None, gny: int | None = None) -> np.ndarray:
+                  gnx: int | None = None, gny: int | None = None,
+                  mean: float | None = None) -> np.ndarray:
     """RHS tile in device order [k][y][x] (float64), mean of the GLOBAL field removed.
 
     (nx, ny) is the global grid unless gnx/gny are given; the tile is
-    [x0, x0+lnx) x [y0, y0+lny).  Global linear index = (k*ny + y)*nx + x.
+    [x0, x0+lnx) x [y0, y0+lny).  Global linear index = (k*ny + y)*nx + x.  `mean` (the
+    global mean, e.g. from all-gathered tile_m_sum values) skips the global pass.
     """
     gnx = nx if gnx is None else gnx
     gny = ny if gny is None else gny
     lnx = gnx if lnx is None else lnx
     lny = gny if lny is None else lny
-    mean = rhs_mean(seed, gnx * gny * nz)
+    if mean is None:
+        mean = rhs_mean(seed, gnx * gny * nz)
     out = np.empty((nz, lny, lnx), dtype=np.float64)
     xs = np.arange(x0, x0 + lnx, dtype=np.uint64)
     for k in range(nz):

@@ -345,3 +345,8 @@ def test_synthetic_rhs_mean_removed_and_decomposition_independent():
     assert np.array_equal(tile, f[:, 8:16, 16:32])
     mean = synth.rhs_mean(0, 32 * 16 * 8)
     assert (f + mean).min() >= -1.0 and (f + mean).max() < 1.0
+    # distributed mean: exact tile sums add up to the global one
+    parts = [synth.tile_m_sum(0, 32, 16, 8, x, y, 16, 8) for x in (0, 16) for y in (0, 8)]
+    assert synth.mean_from_m_sum(sum(parts), 32 * 16 * 8) == mean
+    t2 = synth.rhs_x_fastest(0, 32, 16, 8, x0=16, y0=8, lnx=16, lny=8, mean=mean)
+    assert np.array_equal(t2, tile)
