@@ -131,6 +131,7 @@ class CpuPort:
         O.build()
         self.P = P
         self.o = O.OracleHierarchy.from_problem(P, threads=threads)
+        self.o.set_device_order(False)  # no checker machinery in the timed CPU path
         self.f = synth.x_fastest_to_k_fastest(P.rhs())
 
     def sample(self, iters: int = 2):

@@ -149,6 +149,10 @@ class OracleHierarchy:
     def set_threads(self, t: int):
         lib().tpmgo_set_threads(self._h, t)
 
+    def set_device_order(self, on: bool):
+        """False: fastest CPU schedule for the PCG vector work (baseline timing only)."""
+        lib().tpmgo_set_device_order(self._h, 1 if on else 0)
+
     def coefficients(self, level: int) -> dict:
         nc, nz = self.n_cells(level), self.nz
         out = dict(bh=np.empty(nc), ah=np.empty(nc), xh=np.empty(nc), sh=np.empty(2 * nc),

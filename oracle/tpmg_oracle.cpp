@@ -75,6 +75,7 @@ struct Hier {
   int threads = 1;
   Index cart_nx = 0, cart_ny = 0;  // finest Cartesian dims (0 for generic tables)
   int pcg_fused = -1;              // -1: device rule, 0/1: forced
+  bool device_order = true;        // PCG dots in the device's reduction order (parity mode)
 };
 
 // ColumnMatrix, discretization.hpp:208-231.
@@ -639,6 +640,11 @@ int tpmgo_set_pcg_fused(tpmgo_hier h, int mode) {
   return OK;
 }
 
+int tpmgo_set_device_order(tpmgo_hier h, int on) {
+  h->h.device_order = on != 0;
+  return OK;
+}
+
 int tpmgo_set_threads(tpmgo_hier h, int threads) {
   h->h.threads = threads;
   return OK;
@@ -786,11 +792,31 @@ int tpmgo_pcg_timed(tpmgo_hier H, const double* f, double* x, double tol, int ma
     const Index n = h.lv[L].ncells * h.nz;
     std::vector<double> r(f, f + n), z(n, 0.0), p(n), q(n);
     std::fill(x, x + n, 0.0);
-    const bool dev = h.cart_nx > 0;
+    const bool dev = h.cart_nx > 0 && h.device_order;
     DevOrder d{h.cart_nx, h.cart_ny, h.nz};
+    // Baseline mode (device_order off): plain chunked dots and element-wise updates spread over
+    // the worker threads -- the fastest honest CPU schedule, used when timing the CPU port.
+    const Index nchunk = (n + 65535) / 65536;
+    auto par = [&](auto&& body) {
+      parallel_for(nchunk, h.threads, [&](Index c) {
+        const Index lo = c * 65536, hi = std::min(n, lo + 65536);
+        body(lo, hi);
+      });
+    };
+    auto pdot = [&](const double* a, const double* b) {
+      std::vector<double> part(static_cast<size_t>(nchunk), 0.0);
+      par([&](Index lo, Index hi) {
+        double s = 0.0;
+        for (Index i = lo; i < hi; ++i) s += a[i] * b[i];
+        part[lo / 65536] = s;
+      });
+      double s = 0.0;
+      for (double v : part) s += v;
+      return s;
+    };
     auto dotv = [&](const std::vector<double>& a, const std::vector<double>& b) {
       return dev ? gridstride_dot(d, [&](Index i) { return a[i] * b[i]; })
-                 : dot(n, a.data(), b.data());
+                 : (h.device_order ? dot(n, a.data(), b.data()) : pdot(a.data(), b.data()));
     };
     // The device fuses |r|^2 into the first and r.z into the last finest-level sweep when the
     // finest level runs the tiled TMEM smoother (tpmg_host.cpp pcg_iteration); those partials
@@ -817,16 +843,19 @@ int tpmgo_pcg_timed(tpmgo_hier H, const double* f, double* x, double tol, int ma
     }
     for (int it = 1; it <= max_iter; ++it) {
       apply(h, L, p.data(), q.data());
-      const double pq = dev ? column_dot(d, q.data(), p.data()) : dot(n, p.data(), q.data());
+      const double pq = dev ? column_dot(d, q.data(), p.data())
+                            : (h.device_order ? dot(n, p.data(), q.data()) : pdot(p.data(), q.data()));
       if (!(pq > 0.0)) {
         *solve_status = BREAKDOWN;
         return;
       }
       const double alpha = rho / pq;
-      for (Index i = 0; i < n; ++i) {
-        x[i] += alpha * p[i];
-        r[i] -= alpha * q[i];
-      }
+      par([&](Index lo, Index hi) {
+        for (Index i = lo; i < hi; ++i) {
+          x[i] += alpha * p[i];
+          r[i] -= alpha * q[i];
+        }
+      });
       const double rn = std::sqrt(fused ? column_dot(d, r.data(), r.data()) : dotv(r, r));
       if (res_hist) res_hist[it] = rn;
       *iters = it;
@@ -845,7 +874,9 @@ int tpmgo_pcg_timed(tpmgo_hier H, const double* f, double* x, double tol, int ma
       }
       const double beta = rho_new / rho;
       rho = rho_new;
-      for (Index i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
+      par([&](Index lo, Index hi) {
+        for (Index i = lo; i < hi; ++i) p[i] = z[i] + beta * p[i];
+      });
     }
     *solve_status = NOT_CONVERGED;
   });

@@ -70,6 +70,9 @@ int64_t tpmgo_nz(tpmgo_hier h);
 int tpmgo_set_threads(tpmgo_hier h, int threads);
 /* Reduction order of the PCG dots: -1 = the device's rule (default), 0 = plain, 1 = fused. */
 int tpmgo_set_pcg_fused(tpmgo_hier h, int mode);
+/* 1 (default): PCG dots in the device's reduction order (parity).  0: plain chunked dots and
+ * element-wise updates on the worker threads (CPU-baseline timing). */
+int tpmgo_set_device_order(tpmgo_hier h, int on);
 
 /* Hatted coefficients of a level (assemble_hatted, discretization.hpp:144-184). */
 int tpmgo_get_coefficients(tpmgo_hier h, int level, double* bh, double* ah, double* xh,
