@@ -88,6 +88,8 @@ class OracleHierarchy:
             C.c_int(kw["prolongation"]), C.c_int(kw["restriction"]), C.c_int(kw["nu_pre"]),
             C.c_int(kw["nu_post"]), C.c_int(kw["depth"]), C.c_int(threads), C.byref(h))
         _chk(rc)
+        # mirror the device's smoother switch (jacobi_uses_t4, tpmg_kernels.cu)
+        lib().tpmgo_set_t4(h, 0 if os.environ.get("TPMG_JACOBI_T4", "0") == "0" else 1)
         return cls(h, P.nz)
 
     @classmethod

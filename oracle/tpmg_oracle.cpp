@@ -76,6 +76,7 @@ struct Hier {
   Index cart_nx = 0, cart_ny = 0;  // finest Cartesian dims (0 for generic tables)
   int pcg_fused = -1;              // -1: device rule, 0/1: forced
   bool device_order = true;        // PCG dots in the device's reduction order (parity mode)
+  int t4 = 0;                      // device smoother v4 enabled (TPMG_JACOBI_T4, opt-in)
 };
 
 // ColumnMatrix, discretization.hpp:208-231.
@@ -353,7 +354,10 @@ double gridstride_dot(const DevOrder& d, Val val) {
 
 // fused p.q of the apply kernel: per-column sums over k, then per-CTA trees.
 // descending: the per-column sum runs k = nz-1 .. 0 (sums formed in a back substitution)
-double column_dot(const DevOrder& d, const double* y, const double* u, bool descending = false) {
+// nc = 2: the two-columns-per-thread smoother (k_jacobi_t4): 64x4 tiles, thread t = (tx, ty)
+// holds columns tx and tx+32 and adds its two column sums before the block tree.
+double column_dot(const DevOrder& d, const double* y, const double* u, bool descending = false,
+                  int nc = 1) {
   const Index plane = d.plane();
   std::vector<double> colsum(plane);
   for (Index c = 0; c < plane; ++c) {
@@ -365,7 +369,19 @@ double column_dot(const DevOrder& d, const double* y, const double* u, bool desc
     colsum[c] = a;
   }
   std::vector<double> part;
-  if (d.nx % 32 == 0 && d.ny % 4 == 0) {  // k_apply_tiled: 32x4 tiles, tile order by*gx+bx
+  if (nc == 2) {
+    const Index gx = d.nx / 64, gy = d.ny / 4;
+    part.resize(gx * gy);
+    double acc[128];
+    for (Index by = 0; by < gy; ++by)
+      for (Index bx = 0; bx < gx; ++bx) {
+        for (int t = 0; t < 128; ++t) {
+          const Index c0 = (by * 4 + t / 32) * d.nx + bx * 64 + t % 32;
+          acc[t] = colsum[c0] + colsum[c0 + 32];
+        }
+        part[by * gx + bx] = block_tree(acc, 128);
+      }
+  } else if (d.nx % 32 == 0 && d.ny % 4 == 0) {  // k_apply_t3: 32x4 tiles, order by*gx+bx
     const Index gx = d.nx / 32, gy = d.ny / 4;
     part.resize(gx * gy);
     double acc[128];
@@ -640,6 +656,11 @@ int tpmgo_set_pcg_fused(tpmgo_hier h, int mode) {
   return OK;
 }
 
+int tpmgo_set_t4(tpmgo_hier h, int on) {
+  h->h.t4 = on;
+  return OK;
+}
+
 int tpmgo_set_device_order(tpmgo_hier h, int on) {
   h->h.device_order = on != 0;
   return OK;
@@ -828,6 +849,12 @@ int tpmgo_pcg_timed(tpmgo_hier H, const double* f, double* x, double tol, int ma
                                                 : (h.cart_nx % 32 == 0 && h.cart_ny % 4 == 0 &&
                                                    h.nz % 4 == 0 && cols <= 512 && Lf > 0 &&
                                                    h.nu_pre[Lf] >= 1 && h.nu_post[Lf] >= 1));
+    // ... and those sweeps run two columns per thread (64x4 tiles) when the device's
+    // jacobi_uses_t4 rule holds (tpmg_kernels.cu): 64-wide tiles, even nz, 2 nz <= 256.
+    int cols4 = 32;
+    while (cols4 < 2 * h.nz) cols4 <<= 1;
+    const int nc = (h.t4 != 0 && h.cart_nx > 0 && h.cart_nx % 64 == 0 && h.cart_ny % 4 == 0 &&
+                    h.nz % 4 == 0 && cols4 <= 256) ? 2 : 1;
     const double r0 = std::sqrt(dotv(r, r));
     if (res_hist) res_hist[0] = r0;
     stamp(0);
@@ -856,7 +883,7 @@ int tpmgo_pcg_timed(tpmgo_hier H, const double* f, double* x, double tol, int ma
           r[i] -= alpha * q[i];
         }
       });
-      const double rn = std::sqrt(fused ? column_dot(d, r.data(), r.data()) : dotv(r, r));
+      const double rn = std::sqrt(fused ? column_dot(d, r.data(), r.data(), false, nc) : dotv(r, r));
       if (res_hist) res_hist[it] = rn;
       *iters = it;
       stamp(it);
@@ -867,7 +894,7 @@ int tpmgo_pcg_timed(tpmgo_hier H, const double* f, double* x, double tol, int ma
       }
       std::fill(z.begin(), z.end(), 0.0);
       vcycle(h, L, r.data(), z.data());
-      const double rho_new = fused ? column_dot(d, r.data(), z.data(), true) : dotv(r, z);
+      const double rho_new = fused ? column_dot(d, r.data(), z.data(), true, nc) : dotv(r, z);
       if (!(rho_new > 0.0)) {
         *solve_status = BREAKDOWN;
         return;

@@ -73,6 +73,8 @@ int tpmgo_set_pcg_fused(tpmgo_hier h, int mode);
 /* 1 (default): PCG dots in the device's reduction order (parity).  0: plain chunked dots and
  * element-wise updates on the worker threads (CPU-baseline timing). */
 int tpmgo_set_device_order(tpmgo_hier h, int on);
+/* Mirror of the device's TPMG_JACOBI_T4 switch (two-columns-per-thread smoother). */
+int tpmgo_set_t4(tpmgo_hier h, int on);
 
 /* Hatted coefficients of a level (assemble_hatted, discretization.hpp:144-184). */
 int tpmgo_get_coefficients(tpmgo_hier h, int level, double* bh, double* ah, double* xh,
