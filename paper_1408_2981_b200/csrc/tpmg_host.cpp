@@ -1135,9 +1135,11 @@ int tpmg_time_kernel(tpmg_hierarchy h, int kernel_id, int level, int reps, doubl
     a.alloc(n); b.alloc(n); c.alloc(n);
     const int64_t ncoarse = transfer ? h->lv[level - 1].plane * h->nz : 1;
     cc.alloc(ncoarse);
-    tpmg::launch_fill(h->ctx->launch(), n, a.p, 0.5);
-    tpmg::launch_fill(h->ctx->launch(), n, b.p, 0.25);
-    tpmg::launch_fill(h->ctx->launch(), ncoarse, cc.p, 0.125);
+    // seeded pseudo-random operands (constant fields make A u vanish in places, which would
+    // time the smoother's exact-division fallback instead of its hot path)
+    tpmg::launch_fill_hash(h->ctx->launch(), n, a.p, 1.0, 1);
+    tpmg::launch_fill_hash(h->ctx->launch(), n, b.p, 1.0, 2);
+    tpmg::launch_fill_hash(h->ctx->launch(), ncoarse, cc.p, 1.0, 3);
     auto once = [&] {
       switch (kernel_id) {
         case TPMG_K_APPLY: apply_level(h, level, tpmg::APPLY_AU, a.p, nullptr, c.p); break;

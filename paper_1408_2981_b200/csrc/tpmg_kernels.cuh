@@ -127,6 +127,7 @@ void launch_copy_scalar(const Launch& L, double* s, int dst, int src);
 void launch_kfast_to_xfast(const Launch& L, int64_t ncol, int nz, const double* in, double* out);
 void launch_xfast_to_kfast(const Launch& L, int64_t ncol, int nz, const double* in, double* out);
 void launch_fill(const Launch& L, int64_t n, double* p, double v);
+void launch_fill_hash(const Launch& L, int64_t n, double* p, double v, uint64_t seed);
 
 // Multi-GPU halo packing: face values of u into send buffers [W|E|S|N] of sizes ny*nz,ny*nz,nx*nz,nx*nz.
 void launch_pack_faces(const Launch& L, int nx, int ny, int nz, const double* u, double* send);

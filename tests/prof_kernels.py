@@ -16,7 +16,9 @@ def main():
     names = sys.argv[1:] or list(KERNELS)
     reps = int(os.environ.get("TPMG_REPS", "2"))
     ctx = tpmg.Context()
-    h = tpmg.Hierarchy(ctx, synth.baseline_config(cfg))
+    over = {k.lower(): int(os.environ["TPMG_" + k]) for k in ("NX", "NY", "DEPTH")
+            if "TPMG_" + k in os.environ}
+    h = tpmg.Hierarchy(ctx, synth.baseline_config(cfg, **over))
     for n in names:
         ms = h.time_kernel(KERNELS[n], h.finest, reps=reps)
         print(f"{n}: {ms:.3f} ms", flush=True)
