@@ -53,7 +53,9 @@ def full(rep, out, traffic_json=None):
     want = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
             "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
             "launch__registers_per_thread", "smsp__inst_executed.sum", "launch__grid_size",
-            "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "lts__t_sector_hit_rate.pct"]
+            "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "lts__t_sector_hit_rate.pct",
+            "smsp__issue_active.avg.pct_of_peak_sustained_active",
+            "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
     idx = {w: hdr.index(w) for w in want if w in hdr}
     lines = [f"# ncu --set full summary: `{rep}`", "",
              "| metric | " + " | ".join(f"launch {i}" for i in range(len(rows) - 2)) + " |",
@@ -64,6 +66,14 @@ def full(rep, out, traffic_json=None):
     for w in want:
         if w in idx:
             lines.append(f"| {w} | " + " | ".join(f"{rc[w][0]} {rc[w][1]}".strip() for rc in recs) + " |")
+    # warp-state samples (where the warps wait), top 6 of the last launch
+    stall = [(hdr[i], float(v.replace(",", ""))) for i, v in enumerate(rows[-1])
+             if hdr[i].startswith("smsp__pcsamp_warps_issue_stalled_")
+             and not hdr[i].endswith("_not_issued") and v not in ("", "n/a")]
+    tot = sum(v for _, v in stall) or 1.0
+    lines += ["", "| stall reason (pc samples, last launch) | share |", "|---|---|"]
+    for k, v in sorted(stall, key=lambda x: -x[1])[:6]:
+        lines.append(f"| {k.replace('smsp__pcsamp_warps_issue_stalled_', '')} | {100 * v / tot:.1f}% |")
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
     if traffic_json and recs:
