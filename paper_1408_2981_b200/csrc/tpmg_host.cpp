@@ -157,14 +157,19 @@ struct tpmg_hierarchy_s {
   DevBuf d_bv, d_sv, d_av, d_xv;
   // finest-level PCG / V-cycle work vectors
   DevBuf r, z, p, q, tmp;
+  DevBuf p2;                // second search-direction buffer of the fused A p pass (ping-pong)
+  int pcur = 0;             // which of p / p2 holds the current direction
+  bool fused_ap = false;    // x += a p_old; p = z + b p_old; q = A p in one pass
+  double* pbuf(int i) { return i == 0 ? p.p : p2.p; }
   DevBuf partials, scal;  // reduction partials; scalars s[0..7]
   int* d_err = nullptr;
   double* h_scal = nullptr;  // pinned
   bool use_graphs = true;
   bool pcg_fused = false;  // PCG vector work fused into the finest-level smoother sweeps
   bool fuse_rr = true;     // fused residual + transpose restriction (TPMG_FUSE_RR=0 disables)
-  std::unordered_map<const double*, cudaGraphExec_t> iter_graphs;
-  std::unordered_map<const double*, int64_t> iter_graph_kernels;
+  // one graph per (iterate buffer, direction parity): key = (const char*)x + pcur
+  std::unordered_map<const void*, cudaGraphExec_t> iter_graphs;
+  std::unordered_map<const void*, int64_t> iter_graph_kernels;
   int finest() const { return (int)lv.size() - 1; }
   VertCoef vcoef() const { return VertCoef{d_bv.p, d_sv.p, d_av.p, d_xv.p}; }
   ~tpmg_hierarchy_s() {
@@ -451,16 +456,29 @@ void same_hier(tpmg_hierarchy h, tpmg_field f) {
 // final iteration is applied after the loop (k_pcg_xfinal).  Every element is computed with
 // the same operations as the plain schedule: q = A p, p.q; x += a p, r -= a q, r.r;
 // z = V(r); r.z; p = z + b p.
-void pcg_iteration(tpmg_hierarchy h, double* x, bool first = false) {
+void pcg_iteration(tpmg_hierarchy h, double* x, bool first, int pc) {
   const int L = h->finest();
   const int64_t n = h->lv[L].plane * h->nz;
   tpmg_context ctx = h->ctx;
   if (h->pcg_fused) {
-    if (!first) {
-      tpmg::launch_pcg_px(ctx->launch(), n, h->scal.p, h->z.p, h->p.p, x);
+    if (!first && h->fused_ap) {
+      // direction update and A p in one pass; p_new goes to the other buffer
+      Level& F = h->lv[L];
+      double* po = h->pbuf(pc);
+      int nb = 0;
+      tpmg::launch_pcg_ap(ctx->launch(), h->vcoef(), F.coef(h->nz), h->xi, h->z.p,
+                          tpmg::self_halo(h->z.p, F.nx, F.ny, F.plane), po,
+                          tpmg::self_halo(po, F.nx, F.ny, F.plane), h->pbuf(pc ^ 1), h->q.p, x,
+                          h->scal.p, h->partials.p, &nb);
       tpmg::launch_copy_scalar(ctx->launch(), h->scal.p, 0, 3);
+      finish_dot(h, nb, 1);
+    } else {
+      if (!first) {
+        tpmg::launch_pcg_px(ctx->launch(), n, h->scal.p, h->z.p, h->pbuf(pc), x);
+        tpmg::launch_copy_scalar(ctx->launch(), h->scal.p, 0, 3);
+      }
+      apply_level(h, L, tpmg::APPLY_AU, h->pbuf(pc), nullptr, h->q.p, 1);
     }
-    apply_level(h, L, tpmg::APPLY_AU, h->p.p, nullptr, h->q.p, 1);
     vcycle(h, L, h->r.p, h->z.p, h->tmp.p, true, true);
     return;
   }
@@ -476,17 +494,21 @@ void pcg_iteration(tpmg_hierarchy h, double* x, bool first = false) {
 
 void run_iteration(tpmg_hierarchy h, double* x, bool first) {
   tpmg_context ctx = h->ctx;
+  const int pc = h->pcur;
+  // the fused A p pass moves the direction to the other buffer
+  if (h->pcg_fused && h->fused_ap && !first) h->pcur ^= 1;
   if (!h->use_graphs || (first && h->pcg_fused)) {
-    pcg_iteration(h, x, first);
+    pcg_iteration(h, x, first, pc);
     return;
   }
-  auto it = h->iter_graphs.find(x);
+  const void* key = reinterpret_cast<const char*>(x) + pc;
+  auto it = h->iter_graphs.find(key);
   if (it == h->iter_graphs.end()) {
     cudaGraph_t g;
     const int64_t before = ctx->launches;
     CUDA_CHECK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
     try {
-      pcg_iteration(h, x);
+      pcg_iteration(h, x, false, pc);
     } catch (...) {
       cudaStreamEndCapture(ctx->stream, &g);
       throw;
@@ -497,11 +519,11 @@ void run_iteration(tpmg_hierarchy h, double* x, bool first) {
     cudaGraphExec_t ge;
     CUDA_CHECK(cudaGraphInstantiate(&ge, g, 0));
     cudaGraphDestroy(g);
-    it = h->iter_graphs.emplace(x, ge).first;
-    h->iter_graph_kernels[x] = nk;
+    it = h->iter_graphs.emplace(key, ge).first;
+    h->iter_graph_kernels[key] = nk;
   }
   CUDA_CHECK(cudaGraphLaunch(it->second, ctx->stream));
-  ctx->launches += h->iter_graph_kernels[x];
+  ctx->launches += h->iter_graph_kernels[key];
 }
 
 }  // namespace
@@ -785,6 +807,12 @@ int tpmg_hier_create(tpmg_context ctx, const tpmg_grid_desc* g,
       // TPMG_FUSE_RR=0 selects the split apply + restrict pair (same bits)
       const char* e2 = getenv("TPMG_FUSE_RR");
       h->fuse_rr = !(e2 && atoi(e2) == 0);
+      // fused direction update + A p (single rank: the halo views of z and p_old are the
+      // periodic self views); TPMG_FUSE_AP=0 selects k_pcg_px + the apply kernel
+      const char* e3 = getenv("TPMG_FUSE_AP");
+      h->fused_ap = h->pcg_fused && ctx->world == 1 && !(e3 && atoi(e3) == 0) &&
+                    tpmg::pcg_ap_fusable(h->lv[L].coef(h->nz));
+      if (h->fused_ap) h->p2.alloc(nf);
     }
     *out = h.release();
   });
@@ -1060,6 +1088,7 @@ int tpmg_pcg(tpmg_hierarchy h, tpmg_field f, tpmg_field x, double tol, int max_i
     *solve_status = TPMG_OK;
     if (r0 == 0.0) return;
     vcycle(h, L, h->r.p, h->z.p, h->tmp.p, true);
+    h->pcur = 0;
     CUDA_CHECK(cudaMemcpyAsync(h->p.p, h->z.p, n * 8, cudaMemcpyDeviceToDevice, s));
     dot_into(h, n, h->r.p, h->z.p, 0);
     if (!(read_scalar(h, 0) > 0.0)) {
@@ -1069,7 +1098,7 @@ int tpmg_pcg(tpmg_hierarchy h, tpmg_field f, tpmg_field x, double tol, int max_i
     // fused schedule: the last iteration's x += alpha p is still pending when the loop ends
     auto finish_x = [&] {
       if (h->pcg_fused) {
-        tpmg::launch_pcg_xfinal(ctx->launch(), n, h->scal.p, h->p.p, x->buf.p);
+        tpmg::launch_pcg_xfinal(ctx->launch(), n, h->scal.p, h->pbuf(h->pcur), x->buf.p);
         sync_check(h);
       }
     };

@@ -90,6 +90,13 @@ bool jacobi_fusable(const LevelCoef& C);
 void launch_pcg_px(const Launch& L, int64_t n, const double* s, const double* z, double* p,
                    double* x);
 // x += alpha p   (alpha = s[0]/s[1])
+// Fused x += alpha p_old; p_new = z + beta p_old; q = A p_new (+ per-tile p.q partials):
+// k_pcg_px + launch_apply(DOT) in one pass (tiled levels, z/p_old halos as views).
+bool pcg_ap_fusable(const LevelCoef& C);
+void launch_pcg_ap(const Launch& L, const VertCoef& V, const LevelCoef& C, bool xi,
+                   const double* z, const Halo& Hz, const double* pold, const Halo& Hp,
+                   double* pnew, double* q, double* x, const double* s, double* partials,
+                   int* nblocks);
 void launch_pcg_xfinal(const Launch& L, int64_t n, const double* s, const double* p, double* x);
 
 // coarse = R_sum(fine) (restrict_field, multigrid.hpp:29-43).
