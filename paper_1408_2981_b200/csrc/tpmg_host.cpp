@@ -160,6 +160,7 @@ struct tpmg_hierarchy_s {
   DevBuf p2;                // second search-direction buffer of the fused A p pass (ping-pong)
   int pcur = 0;             // which of p / p2 holds the current direction
   bool fused_ap = false;    // x += a p_old; p = z + b p_old; q = A p in one pass
+  bool q_in_sweep = false;  // ... and q = A p re-formed in the r-update sweep (q not stored)
   double* pbuf(int i) { return i == 0 ? p.p : p2.p; }
   DevBuf partials, scal;  // reduction partials; scalars s[0..7]
   int* d_err = nullptr;
@@ -321,7 +322,9 @@ void apply_level(tpmg_hierarchy h, int l, int mode, const double* u, const doubl
 void sweep(tpmg_hierarchy h, int l, const double* u_in, const double* f, double* out,
            const tpmg::PcgFuse* fz = nullptr, int slot = -1) {
   Level& L = h->lv[l];
-  Halo H = u_in ? exchange(h, l, u_in) : tpmg::self_halo(out, L.nx, L.ny, L.plane);
+  // the haloed input: u, or p when the zero-guess sweep forms q = A p itself
+  Halo H = u_in ? exchange(h, l, u_in)
+                : (fz && fz->p ? exchange(h, l, fz->p) : tpmg::self_halo(out, L.nx, L.ny, L.plane));
   int nb = 0;
   tpmg::launch_jacobi(h->ctx->launch(), h->vcoef(), L.coef(h->nz), h->xi, u_in, H, f, out,
                       h->relax, h->d_err, fz, &nb);
@@ -375,7 +378,7 @@ void fill(tpmg_hierarchy h, double* p, int64_t n, double v) {
 // pcg_fuse (finest level of a fused PCG iteration, f == r): the first sweep from zero also does
 // r -= alpha q and |r|^2 (slot 2); the last post-sweep also does r.z (slot 3).
 void vcycle(tpmg_hierarchy h, int l, const double* f, double* A, double* B, bool zero,
-            bool pcg_fuse = false) {
+            bool pcg_fuse = false, const double* p_dir = nullptr) {
   Level& L = h->lv[l];
   const int64_t n = L.plane * h->nz;
   const int npre = h->nu_pre[l], npost = h->nu_post[l], total = npre + npost;
@@ -384,7 +387,9 @@ void vcycle(tpmg_hierarchy h, int l, const double* f, double* A, double* B, bool
   int s0 = 0;
   tpmg::PcgFuse fz;
   if (pcg_fuse) {
-    fz.q = h->q.p;
+    // with p_dir the pre-sweep forms q = A p_dir itself and q is never stored
+    fz.q = p_dir ? nullptr : h->q.p;
+    fz.p = p_dir;
     fz.r = h->r.p;
     fz.s = h->scal.p;
     fz.partials = h->partials.p;
@@ -468,10 +473,13 @@ void pcg_iteration(tpmg_hierarchy h, double* x, bool first, int pc) {
       int nb = 0;
       tpmg::launch_pcg_ap(ctx->launch(), h->vcoef(), F.coef(h->nz), h->xi, h->z.p,
                           tpmg::self_halo(h->z.p, F.nx, F.ny, F.plane), po,
-                          tpmg::self_halo(po, F.nx, F.ny, F.plane), h->pbuf(pc ^ 1), h->q.p, x,
-                          h->scal.p, h->partials.p, &nb);
+                          tpmg::self_halo(po, F.nx, F.ny, F.plane), h->pbuf(pc ^ 1),
+                          h->q_in_sweep ? nullptr : h->q.p, x, h->scal.p, h->partials.p, &nb);
       tpmg::launch_copy_scalar(ctx->launch(), h->scal.p, 0, 3);
       finish_dot(h, nb, 1);
+      vcycle(h, L, h->r.p, h->z.p, h->tmp.p, true, true,
+             h->q_in_sweep ? h->pbuf(pc ^ 1) : nullptr);
+      return;
     } else {
       if (!first) {
         tpmg::launch_pcg_px(ctx->launch(), n, h->scal.p, h->z.p, h->pbuf(pc), x);
@@ -813,6 +821,8 @@ int tpmg_hier_create(tpmg_context ctx, const tpmg_grid_desc* g,
       h->fused_ap = h->pcg_fused && ctx->world == 1 && !(e3 && atoi(e3) == 0) &&
                     tpmg::pcg_ap_fusable(h->lv[L].coef(h->nz));
       if (h->fused_ap) h->p2.alloc(nf);
+      const char* e4 = getenv("TPMG_Q_IN_SWEEP");
+      h->q_in_sweep = h->fused_ap && !(e4 && atoi(e4) == 0);
     }
     *out = h.release();
   });

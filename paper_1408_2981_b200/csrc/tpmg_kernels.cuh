@@ -76,6 +76,9 @@ struct PcgFuse {
   double* r = nullptr;
   const double* s = nullptr;
   double* partials = nullptr;
+  // zero-guess sweep only: q = A p formed in the sweep from a p patch (halo views in the
+  // launch's Halo) instead of read from q (then q may be null)
+  const double* p = nullptr;
 };
 
 // One block-Jacobi line sweep (smooth, relaxation.hpp:77-97): out = u + relax * T^{-1}(f - A u);
