@@ -286,10 +286,14 @@ def main():
     jac_bytes = 24 * N_dof + 32 * C_cols  # read u, f; write u'; 4 per-column scalars
     achieved = jac_bytes / (t_jac * 1e-3) / 1e9
     kernels = {}
-    for name, kid, by in (("apply", tpmg.K_APPLY, 16 * N_dof + 32 * C_cols),
+    # algorithmic bytes: fields read + written once, 2 B/DOF for a quarter-size coarse field,
+    # 32 B per column of hatted scalars
+    for name, kid, by in (("pcg_direction_Ap", tpmg.K_PCG_DIRECTION, 40 * N_dof + 32 * C_cols),
+                          ("pcg_rupdate_presweep", tpmg.K_PCG_RUPDATE, 32 * N_dof + 32 * C_cols),
                           ("jacobi_zero_guess", tpmg.K_JACOBI_ZERO, 16 * N_dof + 32 * C_cols),
                           ("resid_restrict", tpmg.K_RESID_RESTRICT, 16 * N_dof + 2 * N_dof + 32 * C_cols),
-                          ("prolong_add", tpmg.K_PROLONG_ADD, 16 * N_dof + 2 * N_dof)):
+                          ("prolong_add", tpmg.K_PROLONG_ADD, 16 * N_dof + 2 * N_dof),
+                          ("apply", tpmg.K_APPLY, 16 * N_dof + 32 * C_cols)):
         t = h.time_kernel(kid, h.finest, reps=10)
         kernels[name] = {"ms": t, "GBps": by / (t * 1e-3) / 1e9, "frac": by / (t * 1e-3) / 1e9 / peak}
     # V-cycle alone

@@ -206,7 +206,9 @@ typedef enum tpmg_kernel_id {
   TPMG_K_RESID_RESTRICT = 3,  /* coarse = R (f - A u) as used by the V-cycle */
   TPMG_K_PROLONG_ADD = 4,     /* fine += P coarse                         */
   TPMG_K_RESTRICT = 5,        /* coarse = R fine                          */
-  TPMG_K_RESIDUAL = 6         /* r = f - A u                              */
+  TPMG_K_RESIDUAL = 6,        /* r = f - A u                              */
+  TPMG_K_PCG_DIRECTION = 7,   /* fused PCG pass: x += a p; p = z + b p; A p and p.(A p) */
+  TPMG_K_PCG_RUPDATE = 8      /* fused PCG pre-sweep: r -= a A p, |r|^2, z = smoother(r) */
 } tpmg_kernel_id;
 /* Average device time (CUDA events on the library's stream) of `reps` back-to-back launches
  * of one hot-path kernel on `level` (transfers: `level` is the fine level), on internal

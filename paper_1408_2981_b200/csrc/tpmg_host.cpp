@@ -1171,8 +1171,13 @@ int tpmg_time_kernel(tpmg_hierarchy h, int kernel_id, int level, int reps, doubl
     if (transfer && level < 1) throw Error(TPMG_E_SHAPE, "transfers need a fine level >= 1");
     Level& L = h->lv[level];
     const int64_t n = L.plane * h->nz;
-    DevBuf a, b, c, cc;
+    const bool pcg_kernel = kernel_id == TPMG_K_PCG_DIRECTION || kernel_id == TPMG_K_PCG_RUPDATE;
+    if (pcg_kernel && !(tpmg::jacobi_fusable(h->lv[level].coef(h->nz)) &&
+                        tpmg::pcg_ap_fusable(h->lv[level].coef(h->nz))))
+      throw Error(TPMG_E_SHAPE, "the fused PCG kernels need a tiled level");
+    DevBuf a, b, c, d, cc;
     a.alloc(n); b.alloc(n); c.alloc(n);
+    if (pcg_kernel) d.alloc(n);
     const int64_t ncoarse = transfer ? h->lv[level - 1].plane * h->nz : 1;
     cc.alloc(ncoarse);
     // seeded pseudo-random operands (constant fields make A u vanish in places, which would
@@ -1180,6 +1185,14 @@ int tpmg_time_kernel(tpmg_hierarchy h, int kernel_id, int level, int reps, doubl
     tpmg::launch_fill_hash(h->ctx->launch(), n, a.p, 1.0, 1);
     tpmg::launch_fill_hash(h->ctx->launch(), n, b.p, 1.0, 2);
     tpmg::launch_fill_hash(h->ctx->launch(), ncoarse, cc.p, 1.0, 3);
+    if (pcg_kernel) {
+      tpmg::launch_fill_hash(h->ctx->launch(), n, d.p, 1.0, 4);
+      // PCG scalars rho = 1, p.q = 2, rho_new = 0.5 (alpha = 0.5, beta = 0.5); the r-update
+      // kernel rewrites r in place, so its timing reps start from slightly different r
+      const double sc[4] = {1.0, 2.0, 0.0, 0.5};
+      CUDA_CHECK(cudaMemcpyAsync(h->scal.p, sc, sizeof(sc), cudaMemcpyHostToDevice,
+                                 h->ctx->stream));
+    }
     auto once = [&] {
       switch (kernel_id) {
         case TPMG_K_APPLY: apply_level(h, level, tpmg::APPLY_AU, a.p, nullptr, c.p); break;
@@ -1189,6 +1202,24 @@ int tpmg_time_kernel(tpmg_hierarchy h, int kernel_id, int level, int reps, doubl
         case TPMG_K_RESID_RESTRICT: resid_restrict(h, level, a.p, b.p, cc.p, c.p); break;
         case TPMG_K_PROLONG_ADD: prolong_level(h, level - 1, cc.p, c.p, true); break;
         case TPMG_K_RESTRICT: restrict_plain(h, level, a.p, cc.p); break;
+        case TPMG_K_PCG_DIRECTION: {  // z = a, p_old = b, p_new = c, x = d (finest, tiled)
+          Level& F = h->lv[level];
+          int nb = 0;
+          tpmg::launch_pcg_ap(h->ctx->launch(), h->vcoef(), F.coef(h->nz), h->xi, a.p,
+                              tpmg::self_halo(a.p, F.nx, F.ny, F.plane), b.p,
+                              tpmg::self_halo(b.p, F.nx, F.ny, F.plane), c.p, nullptr, d.p,
+                              h->scal.p, h->partials.p, &nb);
+          break;
+        }
+        case TPMG_K_PCG_RUPDATE: {  // r = a (updated in place), p = b, z = c
+          tpmg::PcgFuse fz;
+          fz.r = a.p;
+          fz.p = b.p;
+          fz.s = h->scal.p;
+          fz.partials = h->partials.p;
+          sweep(h, level, nullptr, a.p, c.p, &fz, 2);
+          break;
+        }
         default: throw Error(TPMG_E_CONFIG, "unknown kernel id");
       }
     };

@@ -21,7 +21,8 @@ from . import _capi
 from ._capi import ContextParams, FactorizedProfiles, GridDesc, MGConfig
 
 K_FASTEST, X_FASTEST = 0, 1
-K_APPLY, K_JACOBI, K_JACOBI_ZERO, K_RESID_RESTRICT, K_PROLONG_ADD, K_RESTRICT, K_RESIDUAL = range(7)
+(K_APPLY, K_JACOBI, K_JACOBI_ZERO, K_RESID_RESTRICT, K_PROLONG_ADD, K_RESTRICT, K_RESIDUAL,
+ K_PCG_DIRECTION, K_PCG_RUPDATE) = range(9)
 LINEAR, INJECTION = 0, 1
 SUMMATION, TRANSPOSE = 0, 1
 OK, E_CONFIG, E_SHAPE, E_NONFINITE, E_FINGERPRINT, E_SINGULAR, E_CAP, E_CUDA, E_NCCL = range(9)
