@@ -191,6 +191,23 @@ int tpmg_norm(tpmg_hierarchy h, tpmg_field a, double* out);
 int tpmg_pcg(tpmg_hierarchy h, tpmg_field f, tpmg_field x, double tol, int max_iter,
              double* res_hist, int* iters, int* solve_status);
 
+/* Preconditioned Richardson (richardson_solve):
+ * x_{k+1} = x_k + M^{-1}(f - A x_k), M^{-1} = mu V-cycles on A e = r from e = 0, x_0 = 0.
+ * Same history / status conventions as tpmg_pcg (divergence guard 1e4). */
+int tpmg_richardson(tpmg_hierarchy h, tpmg_field f, tpmg_field x, double tol, int max_iter,
+                    int mu, double* res_hist, int* iters, int* solve_status);
+
+/* Right-preconditioned BiCGStab, classical single stabilisation (bicgstab_solve,
+ * SPEC.md:412-420, design decisions :443-447): exactly two preconditioner and two operator
+ * applications per full iteration; rho-breakdown (|r^.r| < 1e-30 |r_0|^2) -> TPMG_BREAKDOWN;
+ * convergence is also tested on the intermediate residual s (half step). x_0 = 0. */
+int tpmg_bicgstab(tpmg_hierarchy h, tpmg_field f, tpmg_field x, double tol, int max_iter,
+                  int mu, double* res_hist, int* iters, int* solve_status);
+
+/* Preconditioner and operator applications of the last tpmg_richardson / tpmg_bicgstab call
+ * (the SPEC's per-iteration cost contract). */
+int tpmg_solver_counts(tpmg_hierarchy h, int64_t* n_precond, int64_t* n_matvec);
+
 /* End-to-end solve from host memory: upload f (layout), PCG, download x. */
 int tpmg_pcg_host(tpmg_hierarchy h, const double* f_host, double* x_host, int layout, double tol,
                   int max_iter, double* res_hist, int* iters, int* solve_status);

@@ -216,6 +216,23 @@ class OracleHierarchy:
         return out + (secs[: it.value + 1].copy(),) if seconds else out
 
 
+def _outer(fn, o, f, tol, max_iter, mu):
+    x = np.empty(o.size(o.finest))
+    hist = np.zeros(max_iter + 1)
+    it, st = C.c_int(), C.c_int()
+    _chk(fn(o._h, _p(np.ascontiguousarray(f, dtype=np.float64)), _p(x), C.c_double(tol), max_iter,
+            mu, _p(hist), C.byref(it), C.byref(st)))
+    return x, hist[: it.value + 1].copy(), it.value, st.value
+
+
+def richardson(o: "OracleHierarchy", f, tol=1e-5, max_iter=200, mu=1):
+    return _outer(lib().tpmgo_richardson, o, f, tol, max_iter, mu)
+
+
+def bicgstab(o: "OracleHierarchy", f, tol=1e-5, max_iter=200, mu=1):
+    return _outer(lib().tpmgo_bicgstab, o, f, tol, max_iter, mu)
+
+
 def thomas(diag, upper, lower, rhs):
     x = np.array(rhs, dtype=np.float64, copy=True)
     _chk(lib().tpmgo_thomas(_I64(len(x)), _p(np.ascontiguousarray(diag, dtype=np.float64)),

@@ -909,6 +909,136 @@ int tpmgo_pcg_timed(tpmgo_hier H, const double* f, double* x, double tol, int ma
   });
 }
 
+// Preconditioned Richardson and right-preconditioned BiCGStab (the krylov
+// module the reference specifies but does not ship; design decisions :443-447).  Restated in the
+// operation order of the device drivers (tpmg_host.cpp tpmg_richardson / tpmg_bicgstab) so the
+// strict GPU build is comparable bit for bit: dots in the device's grid-stride tree (Cartesian
+// problems), scalars in double on the host, element-wise updates as k_vec_lin writes them.
+namespace {
+struct Outer {
+  const Hier& h;
+  int L;
+  Index n;
+  bool dev;
+  DevOrder d;
+  explicit Outer(const Hier& hh)
+      : h(hh), L(static_cast<int>(hh.lv.size()) - 1), n(hh.lv[L].ncells * hh.nz),
+        dev(hh.cart_nx > 0 && hh.device_order), d{hh.cart_nx, hh.cart_ny, hh.nz} {}
+  double dotv(const std::vector<double>& a, const std::vector<double>& b) const {
+    return dev ? gridstride_dot(d, [&](Index i) { return a[i] * b[i]; }) : dot(n, a.data(), b.data());
+  }
+  // M^{-1} r: mu V-cycles on A e = r from e = 0
+  void precond(int mu, const std::vector<double>& r, std::vector<double>& e) const {
+    std::fill(e.begin(), e.end(), 0.0);
+    for (int i = 0; i < mu; ++i) vcycle(h, L, r.data(), e.data());
+  }
+};
+}  // namespace
+
+int tpmgo_richardson(tpmgo_hier H, const double* f, double* x, double tol, int max_iter, int mu,
+                     double* res_hist, int* iters, int* solve_status) {
+  return guard([&] {
+    if (max_iter < 0 || mu < 1) throw Error(E_CONFIG, "richardson: max_iter >= 0, mu >= 1");
+    const Outer o(H->h);
+    const Index n = o.n;
+    std::vector<double> r(f, f + n), e(n), xv(n, 0.0), y(n);
+    const double r0 = std::sqrt(o.dotv(r, r));
+    if (res_hist) res_hist[0] = r0;
+    *iters = 0;
+    *solve_status = OK;
+    std::copy(xv.begin(), xv.end(), x);
+    if (r0 == 0.0) return;
+    for (int it = 1; it <= max_iter; ++it) {
+      o.precond(mu, r, e);
+      for (Index i = 0; i < n; ++i) xv[i] = xv[i] + e[i];
+      apply(o.h, o.L, xv.data(), y.data());
+      for (Index i = 0; i < n; ++i) r[i] = f[i] - y[i];
+      const double rn = std::sqrt(o.dotv(r, r));
+      if (res_hist) res_hist[it] = rn;
+      *iters = it;
+      std::copy(xv.begin(), xv.end(), x);
+      if (rn / r0 <= tol) return;
+      if (!(rn / r0 <= 1e4)) {
+        *solve_status = DIVERGED;
+        return;
+      }
+    }
+    *solve_status = NOT_CONVERGED;
+  });
+}
+
+int tpmgo_bicgstab(tpmgo_hier H, const double* f, double* x, double tol, int max_iter, int mu,
+                   double* res_hist, int* iters, int* solve_status) {
+  return guard([&] {
+    if (max_iter < 0 || mu < 1) throw Error(E_CONFIG, "bicgstab: max_iter >= 0, mu >= 1");
+    const Outer o(H->h);
+    const Index n = o.n;
+    std::vector<double> r(f, f + n), rh(f, f + n), p(n, 0.0), v(n, 0.0), ph(n), s(n), sh(n),
+        t(n), xv(n, 0.0);
+    struct Out {  // x is written back on every exit
+      double* x;
+      const std::vector<double>& v;
+      ~Out() { std::copy(v.begin(), v.end(), x); }
+    } out{x, xv};
+    const double r0 = std::sqrt(o.dotv(r, r));
+    if (res_hist) res_hist[0] = r0;
+    *iters = 0;
+    *solve_status = OK;
+    if (r0 == 0.0) return;
+    double rho_prev = 1.0, alpha = 1.0, omega = 1.0;
+    for (int it = 1; it <= max_iter; ++it) {
+      const double rho = o.dotv(rh, r);
+      if (!(std::fabs(rho) >= 1e-30 * r0 * r0)) {
+        *solve_status = BREAKDOWN;
+        return;
+      }
+      const double beta = (rho / rho_prev) * (alpha / omega);
+      for (Index i = 0; i < n; ++i) p[i] = r[i] + beta * (p[i] - omega * v[i]);
+      o.precond(mu, p, ph);
+      apply(o.h, o.L, ph.data(), v.data());
+      const double rv = o.dotv(rh, v);
+      if (!(rv != 0.0)) {
+        *solve_status = BREAKDOWN;
+        return;
+      }
+      alpha = rho / rv;
+      for (Index i = 0; i < n; ++i) s[i] = r[i] - alpha * v[i];
+      const double sn = std::sqrt(o.dotv(s, s));
+      if (sn / r0 <= tol) {
+        for (Index i = 0; i < n; ++i) xv[i] = xv[i] + alpha * ph[i];
+        if (res_hist) res_hist[it] = sn;
+        *iters = it;
+        return;
+      }
+      o.precond(mu, s, sh);
+      apply(o.h, o.L, sh.data(), t.data());
+      const double tt = o.dotv(t, t);
+      const double ts = o.dotv(t, s);
+      if (!(tt != 0.0)) {
+        *solve_status = BREAKDOWN;
+        return;
+      }
+      omega = ts / tt;
+      for (Index i = 0; i < n; ++i) xv[i] = (xv[i] + alpha * ph[i]) + omega * sh[i];
+      for (Index i = 0; i < n; ++i) r[i] = s[i] - omega * t[i];
+      const double rn = std::sqrt(o.dotv(r, r));
+      if (res_hist) res_hist[it] = rn;
+      *iters = it;
+      if (rn / r0 <= tol) return;
+      if (!(rn / r0 <= 1e4)) {
+        *solve_status = DIVERGED;
+        return;
+      }
+      if (!(omega != 0.0)) {
+        *solve_status = BREAKDOWN;
+        return;
+      }
+      rho_prev = rho;
+    }
+    *solve_status = NOT_CONVERGED;
+  });
+}
+
 double tpmgo_dot(int64_t n, const double* a, const double* b) { return dot(n, a, b); }
 
 }  // extern "C"

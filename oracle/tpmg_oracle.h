@@ -108,6 +108,12 @@ int tpmgo_pcg(tpmgo_hier h, const double* f, double* x, double tol, int max_iter
               double* res_hist, int* iters, int* solve_status);
 int tpmgo_pcg_timed(tpmgo_hier h, const double* f, double* x, double tol, int max_iter,
                     double* res_hist, double* seconds, int* iters, int* solve_status);
+/* Preconditioned Richardson / right-preconditioned BiCGStab, mu V-cycles per
+ * preconditioner application, x0 = 0; operation order of the device drivers. */
+int tpmgo_richardson(tpmgo_hier h, const double* f, double* x, double tol, int max_iter, int mu,
+                     double* res_hist, int* iters, int* solve_status);
+int tpmgo_bicgstab(tpmgo_hier h, const double* f, double* x, double tol, int max_iter, int mu,
+                   double* res_hist, int* iters, int* solve_status);
 /* Deterministic dot product used by the oracle's PCG. */
 double tpmgo_dot(int64_t n, const double* a, const double* b);
 

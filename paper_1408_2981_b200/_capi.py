@@ -51,6 +51,11 @@ SIGNATURES = {
     "tpmg_dot": (C.c_int, [_VP, _VP, _VP, _D]),
     "tpmg_norm": (C.c_int, [_VP, _VP, _D]),
     "tpmg_pcg": (C.c_int, [_VP, _VP, _VP, C.c_double, C.c_int, _D, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "tpmg_richardson": (C.c_int, [_VP, _VP, _VP, C.c_double, C.c_int, C.c_int, _D, C.POINTER(C.c_int),
+                                  C.POINTER(C.c_int)]),
+    "tpmg_bicgstab": (C.c_int, [_VP, _VP, _VP, C.c_double, C.c_int, C.c_int, _D, C.POINTER(C.c_int),
+                                C.POINTER(C.c_int)]),
+    "tpmg_solver_counts": (C.c_int, [_VP, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "tpmg_pcg_host": (C.c_int, [_VP, _D, _D, C.c_int, C.c_double, C.c_int, _D, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "tpmg_kernel_launch_count": (C.c_int, [_VP, C.POINTER(C.c_int64)]),
     "tpmg_set_use_graphs": (C.c_int, [_VP, C.c_int]),

@@ -161,6 +161,10 @@ struct tpmg_hierarchy_s {
   int pcur = 0;             // which of p / p2 holds the current direction
   bool fused_ap = false;    // x += a p_old; p = z + b p_old; q = A p in one pass
   bool q_in_sweep = false;  // ... and q = A p re-formed in the r-update sweep (q not stored)
+  // Richardson / BiCGStab work vectors (allocated on first use) and operation counts of the
+  // last outer solve (2 preconditioner + 2 operator applications per BiCGStab step)
+  DevBuf k_rh, k_p, k_v, k_ph, k_s, k_sh, k_t;
+  int64_t n_precond = 0, n_matvec = 0;
   double* pbuf(int i) { return i == 0 ? p.p : p2.p; }
   DevBuf partials, scal;  // reduction partials; scalars s[0..7]
   int* d_err = nullptr;
@@ -1155,6 +1159,153 @@ int tpmg_pcg_host(tpmg_hierarchy h, const double* f_host, double* x_host, int la
   tpmg_field_destroy(f);
   tpmg_field_destroy(x);
   return rc;
+}
+
+// ---- Richardson and right-preconditioned BiCGStab -------------------------
+// Preconditioner M^{-1}: mu V-cycles on A e = r from e = 0; the finest-level
+// operator and V-cycle are the PCG ones.  Dot products are the deterministic device dots, the
+// scalars are formed on the host in IEEE double, element-wise updates in a fixed order
+// (k_vec_lin), so the CPU restatement (tpmgo_richardson / tpmgo_bicgstab) is bitwise equal.
+namespace {
+void precondition(tpmg_hierarchy h, int mu, const double* r, double* e) {
+  const int L = h->finest();
+  for (int i = 0; i < mu; ++i) vcycle(h, L, r, e, h->tmp.p, i == 0);
+  ++h->n_precond;
+}
+double dot_now(tpmg_hierarchy h, int64_t n, const double* a, const double* b) {
+  dot_into(h, n, a, b, 4);
+  return read_scalar(h, 4);
+}
+}  // namespace
+
+int tpmg_richardson(tpmg_hierarchy h, tpmg_field f, tpmg_field x, double tol, int max_iter,
+                    int mu, double* res_hist, int* iters, int* solve_status) {
+  return guard(h->ctx, [&] {
+    same_hier(h, f); same_hier(h, x);
+    const int L = h->finest();
+    if (f->level != L || x->level != L) throw Error(TPMG_E_SHAPE, "richardson: fields must be finest");
+    if (max_iter < 0 || mu < 1) throw Error(TPMG_E_CONFIG, "richardson: max_iter >= 0, mu >= 1");
+    tpmg_context ctx = h->ctx;
+    const int64_t n = f->buf.n;
+    cudaStream_t st = ctx->stream;
+    h->n_precond = h->n_matvec = 0;
+    if (!h->k_rh.p) h->k_rh.alloc(n);
+    double* e = h->k_rh.p;
+    CUDA_CHECK(cudaMemsetAsync(x->buf.p, 0, n * 8, st));
+    CUDA_CHECK(cudaMemcpyAsync(h->r.p, f->buf.p, n * 8, cudaMemcpyDeviceToDevice, st));
+    const double r0 = std::sqrt(dot_now(h, n, h->r.p, h->r.p));
+    if (res_hist) res_hist[0] = r0;
+    *iters = 0;
+    *solve_status = TPMG_OK;
+    if (r0 == 0.0) return;
+    for (int it = 1; it <= max_iter; ++it) {
+      precondition(h, mu, h->r.p, e);                                   // e = M^{-1} r
+      tpmg::launch_vec_lin(ctx->launch(), tpmg::VL_ADD, n, x->buf.p, e, nullptr, 0.0, 0.0);
+      apply_level(h, L, tpmg::APPLY_RESID, x->buf.p, f->buf.p, h->r.p); // r = f - A x
+      ++h->n_matvec;
+      const double rn = std::sqrt(dot_now(h, n, h->r.p, h->r.p));
+      if (res_hist) res_hist[it] = rn;
+      *iters = it;
+      if (rn / r0 <= tol) return;
+      if (!(rn / r0 <= 1e4)) {
+        *solve_status = TPMG_DIVERGED;
+        return;
+      }
+    }
+    *solve_status = TPMG_NOT_CONVERGED;
+  });
+}
+
+int tpmg_bicgstab(tpmg_hierarchy h, tpmg_field f, tpmg_field x, double tol, int max_iter,
+                  int mu, double* res_hist, int* iters, int* solve_status) {
+  return guard(h->ctx, [&] {
+    same_hier(h, f); same_hier(h, x);
+    const int L = h->finest();
+    if (f->level != L || x->level != L) throw Error(TPMG_E_SHAPE, "bicgstab: fields must be finest");
+    if (max_iter < 0 || mu < 1) throw Error(TPMG_E_CONFIG, "bicgstab: max_iter >= 0, mu >= 1");
+    tpmg_context ctx = h->ctx;
+    const int64_t n = f->buf.n;
+    cudaStream_t st = ctx->stream;
+    h->n_precond = h->n_matvec = 0;
+    for (DevBuf* b : {&h->k_rh, &h->k_p, &h->k_v, &h->k_ph, &h->k_s, &h->k_sh, &h->k_t})
+      if (!b->p) b->alloc(n);
+    double *r = h->r.p, *rh = h->k_rh.p, *p = h->k_p.p, *v = h->k_v.p, *ph = h->k_ph.p;
+    double *sv = h->k_s.p, *sh = h->k_sh.p, *t = h->k_t.p, *xp = x->buf.p;
+    CUDA_CHECK(cudaMemsetAsync(xp, 0, n * 8, st));
+    CUDA_CHECK(cudaMemcpyAsync(r, f->buf.p, n * 8, cudaMemcpyDeviceToDevice, st));
+    CUDA_CHECK(cudaMemcpyAsync(rh, f->buf.p, n * 8, cudaMemcpyDeviceToDevice, st));  // r^ = r_0
+    CUDA_CHECK(cudaMemsetAsync(p, 0, n * 8, st));
+    CUDA_CHECK(cudaMemsetAsync(v, 0, n * 8, st));
+    const double r0 = std::sqrt(dot_now(h, n, r, r));
+    if (res_hist) res_hist[0] = r0;
+    *iters = 0;
+    *solve_status = TPMG_OK;
+    if (r0 == 0.0) return;
+    double rho_prev = 1.0, alpha = 1.0, omega = 1.0;
+    const auto lin = [&](int op, double* y, const double* a, const double* b, double s1, double s2) {
+      tpmg::launch_vec_lin(ctx->launch(), op, n, y, a, b, s1, s2);
+    };
+    for (int it = 1; it <= max_iter; ++it) {
+      const double rho = dot_now(h, n, rh, r);
+      if (!(std::fabs(rho) >= 1e-30 * r0 * r0)) {  // rho-breakdown
+        *solve_status = TPMG_BREAKDOWN;
+        return;
+      }
+      const double beta = (rho / rho_prev) * (alpha / omega);
+      lin(tpmg::VL_P, p, r, v, beta, omega);                   // p = r + beta (p - omega v)
+      CUDA_CHECK(cudaMemsetAsync(ph, 0, n * 8, st));
+      precondition(h, mu, p, ph);                              // p^ = M^{-1} p
+      apply_level(h, L, tpmg::APPLY_AU, ph, nullptr, v);      // v = A p^
+      ++h->n_matvec;
+      const double rv = dot_now(h, n, rh, v);
+      if (!(rv != 0.0)) {
+        *solve_status = TPMG_BREAKDOWN;
+        return;
+      }
+      alpha = rho / rv;
+      lin(tpmg::VL_AXMY, sv, r, v, alpha, 0.0);               // s = r - alpha v
+      const double sn = std::sqrt(dot_now(h, n, sv, sv));
+      if (sn / r0 <= tol) {                                    // converged at the half step
+        lin(tpmg::VL_AXPY, xp, ph, nullptr, alpha, 0.0);       // x = x + alpha p^
+        if (res_hist) res_hist[it] = sn;
+        *iters = it;
+        return;
+      }
+      CUDA_CHECK(cudaMemsetAsync(sh, 0, n * 8, st));
+      precondition(h, mu, sv, sh);                             // s^ = M^{-1} s
+      apply_level(h, L, tpmg::APPLY_AU, sh, nullptr, t);      // t = A s^
+      ++h->n_matvec;
+      const double tt = dot_now(h, n, t, t);
+      const double ts = dot_now(h, n, t, sv);
+      if (!(tt != 0.0)) {
+        *solve_status = TPMG_BREAKDOWN;
+        return;
+      }
+      omega = ts / tt;
+      lin(tpmg::VL_X2, xp, ph, sh, alpha, omega);              // x = (x + alpha p^) + omega s^
+      lin(tpmg::VL_AXMY, r, sv, t, omega, 0.0);                // r = s - omega t
+      const double rn = std::sqrt(dot_now(h, n, r, r));
+      if (res_hist) res_hist[it] = rn;
+      *iters = it;
+      if (rn / r0 <= tol) return;
+      if (!(rn / r0 <= 1e4)) {
+        *solve_status = TPMG_DIVERGED;
+        return;
+      }
+      if (!(omega != 0.0)) {
+        *solve_status = TPMG_BREAKDOWN;
+        return;
+      }
+      rho_prev = rho;
+    }
+    *solve_status = TPMG_NOT_CONVERGED;
+  });
+}
+
+int tpmg_solver_counts(tpmg_hierarchy h, int64_t* n_precond, int64_t* n_matvec) {
+  *n_precond = h->n_precond;
+  *n_matvec = h->n_matvec;
+  return TPMG_OK;
 }
 
 int tpmg_kernel_launch_count(tpmg_context ctx, int64_t* out) {

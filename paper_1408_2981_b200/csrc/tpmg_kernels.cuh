@@ -100,6 +100,10 @@ void launch_pcg_ap(const Launch& L, const VertCoef& V, const LevelCoef& C, bool 
                    const double* z, const Halo& Hz, const double* pold, const Halo& Hp,
                    double* pnew, double* q, double* x, const double* s, double* partials,
                    int* nblocks);
+// Richardson / BiCGStab element-wise updates (see k_vec_lin for the exact expressions).
+enum VecLinOp { VL_P = 0, VL_AXMY = 1, VL_X2 = 2, VL_AXPY = 3, VL_ADD = 4 };
+void launch_vec_lin(const Launch& L, int op, int64_t n, double* y, const double* a,
+                    const double* b, double s1, double s2);
 void launch_pcg_xfinal(const Launch& L, int64_t n, const double* s, const double* p, double* x);
 
 // coarse = R_sum(fine) (restrict_field, multigrid.hpp:29-43).

@@ -117,7 +117,22 @@ class Context:
         self.lib.tpmg_kernel_launch_count(self._h, C.byref(n))
         return n.value
 
+    # Handles are freed parent-last whatever order the garbage collector finalises them in
+    # (objects in a reference cycle, e.g. held by a traceback, are finalised in arbitrary
+    # order): a parent closed while children are alive only marks itself, and the last child
+    # to close frees it.
+    _live_children = 0
+    _pending_close = False
+
+    def _child_closed(self):
+        self._live_children -= 1
+        if self._pending_close and self._live_children == 0:
+            self.close()
+
     def close(self):
+        if self._live_children > 0:
+            self._pending_close = True
+            return
         if self._h is not None:
             self.lib.tpmg_finalize(self._h)
             self._h = None
@@ -141,6 +156,7 @@ class Field:
         h = C.c_void_p()
         hier.ctx._check(hier.lib.tpmg_field_create(hier._h, level, C.byref(h)))
         self._h = h
+        hier._live_children += 1
         self.nx, self.ny, self.nz = hier.level_shape(level)[:3]
 
     @property
@@ -182,6 +198,7 @@ class Field:
         if getattr(self, "_h", None) is not None:
             self.hier.lib.tpmg_field_destroy(self._h)
             self._h = None
+            self.hier._child_closed()
 
     def __del__(self):
         # at interpreter shutdown the destruction order of handles is arbitrary: leave the
@@ -220,6 +237,7 @@ class Hierarchy:
         ctx._check(self.lib.tpmg_hier_create(ctx._h, C.byref(grid), C.byref(prof),
                                              C.c_double(P.omega), C.byref(cfg), C.byref(h)))
         self._h = h
+        ctx._live_children += 1
         self._keep = None
         self.problem = P
         n = C.c_int()
@@ -255,10 +273,22 @@ class Hierarchy:
     def set_use_graphs(self, on: bool):
         self.lib.tpmg_set_use_graphs(self._h, 1 if on else 0)
 
+    _live_children = 0
+    _pending_close = False
+
+    def _child_closed(self):
+        self._live_children -= 1
+        if self._pending_close and self._live_children == 0:
+            self.close()
+
     def close(self):
+        if self._live_children > 0:  # fields still alive: the last one closes this
+            self._pending_close = True
+            return
         if getattr(self, "_h", None) is not None:
             self.lib.tpmg_hier_destroy(self._h)
             self._h = None
+            self.ctx._child_closed()
 
     def __del__(self):
         # at interpreter shutdown the destruction order of handles is arbitrary: leave the
@@ -340,6 +370,34 @@ def pcg_solve(h: Hierarchy, f: Field, x: Field, tol: float, max_iter: int = 500)
     h.ctx._check(h.lib.tpmg_pcg(h._h, f._h, x._h, C.c_double(tol), max_iter, _p(hist),
                                 C.byref(it), C.byref(st)))
     return SolveResult(it.value, st.value, hist[: it.value + 1].copy(), time.perf_counter() - t0)
+
+
+def _outer_solve(fn, h: Hierarchy, f: Field, x: Field, tol: float, max_iter: int, mu: int):
+    hist = np.zeros(max_iter + 1)
+    it, st = C.c_int(), C.c_int()
+    t0 = time.perf_counter()
+    h.ctx._check(fn(h._h, f._h, x._h, C.c_double(tol), max_iter, mu, _p(hist), C.byref(it),
+                    C.byref(st)))
+    return SolveResult(it.value, st.value, hist[: it.value + 1].copy(), time.perf_counter() - t0)
+
+
+def richardson_solve(h: Hierarchy, f: Field, x: Field, tol: float = 1e-5, max_iter: int = 500,
+                     mu: int = 1) -> SolveResult:
+    """Preconditioned Richardson, mu V-cycles per step (richardson_solve)."""
+    return _outer_solve(h.lib.tpmg_richardson, h, f, x, tol, max_iter, mu)
+
+
+def bicgstab_solve(h: Hierarchy, f: Field, x: Field, tol: float = 1e-5, max_iter: int = 500,
+                   mu: int = 1) -> SolveResult:
+    """Right-preconditioned BiCGStab (bicgstab_solve)."""
+    return _outer_solve(h.lib.tpmg_bicgstab, h, f, x, tol, max_iter, mu)
+
+
+def solver_counts(h: Hierarchy):
+    """(preconditioner applications, operator applications) of the last outer solve."""
+    a, b = C.c_int64(), C.c_int64()
+    h.ctx._check(h.lib.tpmg_solver_counts(h._h, C.byref(a), C.byref(b)))
+    return a.value, b.value
 
 
 def pcg_solve_host(h: Hierarchy, f_host: np.ndarray, tol: float, max_iter: int = 500,
