@@ -146,4 +146,27 @@ inline ConvergenceHistory pcg_solve(const Hierarchy& h, const Field& f, Field& x
   return c;
 }
 
+// richardson_solve / bicgstab_solve with mu V-cycles per preconditioner
+// application (SolverConfig::mu).
+inline ConvergenceHistory richardson_solve(const Hierarchy& h, const Field& f, Field& x,
+                                           double tol = 1e-5, int max_iter = 500, int mu = 1) {
+  ConvergenceHistory c;
+  c.res_norm.assign(static_cast<size_t>(max_iter) + 1, 0.0);
+  check(tpmg_richardson(h.get(), f.get(), x.get(), tol, max_iter, mu, c.res_norm.data(),
+                        &c.iterations, &c.status),
+        h.context());
+  c.res_norm.resize(static_cast<size_t>(c.iterations) + 1);
+  return c;
+}
+inline ConvergenceHistory bicgstab_solve(const Hierarchy& h, const Field& f, Field& x,
+                                         double tol = 1e-5, int max_iter = 500, int mu = 1) {
+  ConvergenceHistory c;
+  c.res_norm.assign(static_cast<size_t>(max_iter) + 1, 0.0);
+  check(tpmg_bicgstab(h.get(), f.get(), x.get(), tol, max_iter, mu, c.res_norm.data(),
+                      &c.iterations, &c.status),
+        h.context());
+  c.res_norm.resize(static_cast<size_t>(c.iterations) + 1);
+  return c;
+}
+
 }  // namespace tpmg_b200
