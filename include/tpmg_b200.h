@@ -103,6 +103,23 @@ typedef struct tpmg_factorized_profiles {
   const double* alpha_s_s; /* 2*nx*ny: east edges, then north edges */
 } tpmg_factorized_profiles;
 
+/* Full (non-factorised) profiles, the reference's ProfileSet (profiles.hpp:182-192): dense
+ * arrays in the reference's Matrix order (column-major, level k fastest).  GLOBAL, like the
+ * factorised horizontal arrays. */
+typedef struct tpmg_full_profiles {
+  const double* beta;    /* nz x nx*ny                                    */
+  const double* alpha_s; /* nz x 2*nx*ny: east edges, then north edges    */
+  const double* alpha_r; /* (nz+1) x nx*ny                                */
+  const double* xi_r;    /* (nz+1) x nx*ny, NULL = no vertical advection  */
+} tpmg_full_profiles;
+
+/* Coefficient storage of a hierarchy (HattedComponent, discretization.hpp:32-48). */
+typedef enum tpmg_coef_mode {
+  TPMG_COEF_FACTORIZED = 0, /* TPMG(tensor): every component vertical x horizontal      */
+  TPMG_COEF_PARTIAL = 1,    /* TPMG(partial): alpha_r dense (MixedProfileSet)            */
+  TPMG_COEF_FULL = 2        /* TPMG(full): every component dense (ProfileSet)            */
+} tpmg_coef_mode;
+
 /* Arguments of build_hierarchy_coefficients, multigrid.hpp:242-272. */
 typedef struct tpmg_mg_config {
   int smoother;     /* tpmg_smoother_kind */
@@ -141,6 +158,20 @@ int tpmg_plan_decomposition(int64_t nx, int64_t ny, int px, int py, int rank, in
 int tpmg_hier_create(tpmg_context ctx, const tpmg_grid_desc* grid,
                      const tpmg_factorized_profiles* profiles, double omega,
                      const tpmg_mg_config* cfg, tpmg_hierarchy* out);
+/* build_hierarchy_coefficients with a MixedProfileSet (profiles.hpp:225-233,
+ * build_partial_factorization :237-249): `profiles` supplies beta, alpha_s and xi_r (its
+ * alpha_r parts are unused), `alpha_r` is the full (nz+1) x nx*ny field (k fastest). */
+int tpmg_hier_create_partial(tpmg_context ctx, const tpmg_grid_desc* grid,
+                             const tpmg_factorized_profiles* profiles, const double* alpha_r,
+                             double omega, const tpmg_mg_config* cfg, tpmg_hierarchy* out);
+/* build_hierarchy_coefficients with a full ProfileSet: every hatted component dense per
+ * level (assemble_hatted, discretization.hpp:104-141; restrict_profiles multigrid.hpp:146-156).
+ * The device reads +8 B/DOF (partial) or +48 B/DOF (+56 with xi) of coefficients per
+ * operator row: alpha_s is stored per cell for its four edges, so no coefficient halo. */
+int tpmg_hier_create_full(tpmg_context ctx, const tpmg_grid_desc* grid,
+                          const tpmg_full_profiles* profiles, double omega,
+                          const tpmg_mg_config* cfg, tpmg_hierarchy* out);
+int tpmg_hier_coef_mode(tpmg_hierarchy h, int* mode);
 int tpmg_hier_destroy(tpmg_hierarchy h);
 int tpmg_hier_n_levels(tpmg_hierarchy h, int* n_levels);
 /* Local tile shape and global offset of `level` on this rank. */

@@ -81,12 +81,22 @@ class OracleHierarchy:
         if getattr(P, "xi_r_r", None) is not None:
             xr = np.ascontiguousarray(P.xi_r_r, dtype=np.float64)
             xs = np.ascontiguousarray(P.xi_r_s, dtype=np.float64)
-        rc = lib().tpmgo_cart_create(
-            _I64(P.nx), _I64(P.ny), C.c_double(P.hx), C.c_double(P.hy), _I64(P.nz),
-            _p(keep[0]), _p(keep[1]), _p(keep[2]), _p(keep[3]), _p(xr), _p(keep[4]), _p(keep[5]),
-            _p(xs), _p(keep[6]), C.c_double(P.omega), C.c_double(kw["relax"]),
-            C.c_int(kw["prolongation"]), C.c_int(kw["restriction"]), C.c_int(kw["nu_pre"]),
-            C.c_int(kw["nu_post"]), C.c_int(kw["depth"]), C.c_int(threads), C.byref(h))
+        args = (_I64(P.nx), _I64(P.ny), C.c_double(P.hx), C.c_double(P.hy), _I64(P.nz),
+                _p(keep[0]), _p(keep[1]), _p(keep[2]), _p(keep[3]), _p(xr), _p(keep[4]),
+                _p(keep[5]), _p(xs), _p(keep[6]), C.c_double(P.omega), C.c_double(kw["relax"]),
+                C.c_int(kw["prolongation"]), C.c_int(kw["restriction"]), C.c_int(kw["nu_pre"]),
+                C.c_int(kw["nu_post"]), C.c_int(kw["depth"]), C.c_int(threads), C.byref(h))
+        coef = getattr(P, "coef", "factorized")
+        if coef == "factorized":
+            rc = lib().tpmgo_cart_create(*args)
+        else:
+            d = {k: (None if v is None else np.ascontiguousarray(v, dtype=np.float64))
+                 for k, v in P.dense.items()}
+            keep += [v for v in d.values() if v is not None]
+            mode = 1 if coef == "partial" else 2
+            rc = lib().tpmgo_cart_create_dense(
+                C.c_int(mode), _p(d["beta"]), _p(d["alpha_s"]), _p(d["alpha_r"]), _p(d["xi_r"]),
+                *args)
         _chk(rc)
         # mirror the device's smoother switch (jacobi_uses_t4, tpmg_kernels.cu)
         lib().tpmgo_set_t4(h, 0 if os.environ.get("TPMG_JACOBI_T4", "0") == "0" else 1)

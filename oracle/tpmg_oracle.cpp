@@ -61,6 +61,9 @@ struct Level {
   std::vector<Index> children;    // children of THIS level's cells on level+1: T*nchild + j
   // separable hatted horizontal factors (HattedComponent::horiz, discretization.hpp:32-48)
   std::vector<double> bh, ah, xh, sh;
+  // dense hatted components (HattedComponent::dense) of the partial / full modes, [k][T]
+  // (alpha_s: [k][e]); empty when unused
+  std::vector<double> bd, ard, xid, sd;
 };
 
 struct Hier {
@@ -77,6 +80,7 @@ struct Hier {
   int pcg_fused = -1;              // -1: device rule, 0/1: forced
   bool device_order = true;        // PCG dots in the device's reduction order (parity mode)
   int t4 = 0;                      // device smoother v4 enabled (TPMG_JACOBI_T4, opt-in)
+  int cm = 0;                      // 0 factorised, 1 partial (alpha_r dense), 2 full
 };
 
 // ColumnMatrix, discretization.hpp:208-231.
@@ -89,23 +93,29 @@ struct Col {
 
 // build_column, discretization.hpp:235-251 (HattedComponent::operator() = vert[k]*horiz[j],
 // discretization.hpp:39-41).
+// HattedComponent::operator()(k, j) (discretization.hpp:39-41): the separable product, or the
+// dense entry for the components the partial / full modes store in full.
 void build_column(const Hier& h, const Level& L, Index T, Col& c) {
-  const Index nr = h.nz;
+  const Index nr = h.nz, nc = L.ncells;
   c.resize(nr, h.nnb);
   const double ahT = L.ah[T], xhT = L.xh[T], bhT = L.bh[T];
+  auto alpha_r = [&](Index k) { return h.cm ? L.ard[k * nc + T] : h.av[k] * ahT; };
+  auto xi_r = [&](Index k) { return h.cm == 2 ? (L.xid.empty() ? 0.0 : L.xid[k * nc + T]) : h.xv[k] * xhT; };
   for (Index k = 0; k < nr; ++k) {
-    c.upper[k] = -(h.av[k + 1] * ahT) - h.xv[k + 1] * xhT;
-    c.lower[k] = -(h.av[k] * ahT) + h.xv[k] * xhT;
+    c.upper[k] = -alpha_r(k + 1) - xi_r(k + 1);
+    c.lower[k] = -alpha_r(k) + xi_r(k);
   }
   for (int j = 0; j < h.nnb; ++j) {
     const Index e = L.cedge[T * h.nnb + j];
-    for (Index k = 0; k < nr; ++k) c.nb[j * nr + k] = -(h.sv[k] * L.sh[e]);
+    for (Index k = 0; k < nr; ++k)
+      c.nb[j * nr + k] = -(h.cm == 2 ? L.sd[k * L.nedges + e] : h.sv[k] * L.sh[e]);
   }
   for (Index k = 0; k < nr; ++k) {
     // Eigen row(k).sum() of the n_r x nnb neighbour block: ((n0 + n1) + n2) + ...
     double s = c.nb[k];
     for (int j = 1; j < h.nnb; ++j) s = s + c.nb[j * nr + k];
-    c.diag[k] = h.bv[k] * bhT - ((c.upper[k] + c.lower[k]) + s);
+    const double beta = h.cm == 2 ? L.bd[k * nc + T] : h.bv[k] * bhT;
+    c.diag[k] = beta - ((c.upper[k] + c.lower[k]) + s);
   }
 }
 
@@ -439,12 +449,16 @@ extern "C" {
 
 const char* tpmgo_last_error(void) { return g_last_error.c_str(); }
 
-int tpmgo_cart_create(int64_t nx, int64_t ny, double hx, double hy, int64_t nz,
-                      const double* z, const double* beta_r, const double* alpha_s_r,
-                      const double* alpha_r_r, const double* xi_r_r, const double* beta_s,
-                      const double* alpha_r_s, const double* xi_r_s, const double* alpha_s_s,
-                      double omega, double relax, int prolongation, int restriction, int nu_pre,
-                      int nu_post, int depth, int threads, tpmgo_hier* out) {
+namespace {
+// cm: 0 factorised profiles; 1 partial (dense alpha_r `da`); 2 full (dense db, ds, da, dx; the
+// factorised arguments may be null).  Dense inputs in the reference's Matrix order (k fastest).
+int cart_create_impl(int cm, const double* db, const double* ds, const double* da,
+                     const double* dx, int64_t nx, int64_t ny, double hx, double hy, int64_t nz,
+                     const double* z, const double* beta_r, const double* alpha_s_r,
+                     const double* alpha_r_r, const double* xi_r_r, const double* beta_s,
+                     const double* alpha_r_s, const double* xi_r_s, const double* alpha_s_s,
+                     double omega, double relax, int prolongation, int restriction, int nu_pre,
+                     int nu_post, int depth, int threads, tpmgo_hier* out) {
   return guard([&] {
     if (nx < 1 || ny < 1 || nz < 1) throw Error(E_CONFIG, "grid dimensions must be positive");
     if (!(hx > 0.0) || !(hy > 0.0)) throw Error(E_CONFIG, "cell widths must be positive");
@@ -474,6 +488,17 @@ int tpmgo_cart_create(int64_t nx, int64_t ny, double hx, double hy, int64_t nz,
     }
     const Index ncf = nx * ny;
     check_finite(z, nz + 1, "z_faces");
+    std::vector<double> zero_v(nz + 1, 0.0), zero_h(2 * ncf, 0.0);
+    if (cm == 2) {  // full: the factorised parts are not used
+      beta_r = alpha_s_r = alpha_r_r = zero_v.data();
+      beta_s = alpha_r_s = alpha_s_s = zero_h.data();
+      xi_r_r = xi_r_s = nullptr;
+      check_finite(db, nz * ncf, "beta");
+      check_finite(ds, nz * 2 * ncf, "alpha_s");
+      check_finite(da, (nz + 1) * ncf, "alpha_r");
+      if (dx) check_finite(dx, (nz + 1) * ncf, "xi_r");
+    }
+    if (cm == 1) check_finite(da, (nz + 1) * ncf, "alpha_r (full)");
     check_finite(beta_r, nz, "beta_r");
     check_finite(alpha_s_r, nz, "alpha_s_r");
     check_finite(alpha_r_r, nz + 1, "alpha_r_r");
@@ -482,6 +507,19 @@ int tpmgo_cart_create(int64_t nx, int64_t ny, double hx, double hy, int64_t nz,
     check_finite(alpha_r_s, ncf, "alpha_r_s");
     if (xi_r_s) check_finite(xi_r_s, ncf, "xi_r_s");
     check_finite(alpha_s_s, 2 * ncf, "alpha_s_s");
+    // dense profiles [k][global cell] (alpha_s: [k][edge])
+    std::vector<double> Da, Db, Dx, Ds;
+    auto to_kc = [&](const double* in, Index rows, Index cols, std::vector<double>& o) {
+      o.resize(rows * cols);
+      for (Index c = 0; c < cols; ++c)
+        for (Index k = 0; k < rows; ++k) o[k * cols + c] = in[c * rows + k];
+    };
+    if (cm >= 1) to_kc(da, nz + 1, ncf, Da);
+    if (cm == 2) {
+      to_kc(db, nz, ncf, Db);
+      to_kc(ds, nz, 2 * ncf, Ds);
+      if (dx) to_kc(dx, nz + 1, ncf, Dx);
+    }
 
     auto* H = new tpmgo_hier_s;
     Hier& h = H->h;
@@ -492,6 +530,7 @@ int tpmgo_cart_create(int64_t nx, int64_t ny, double hx, double hy, int64_t nz,
     h.prolongation = prolongation;
     h.restriction = restriction;
     h.threads = threads;
+    h.cm = cm;
     // Cartesian corner child (a,b) = a + 2b blends the x-side and y-side coarse neighbours
     // (directions W=0, E=1, S=2, N=3) -- analogue of multigrid.hpp:91-95.
     h.cart_nx = nx;
@@ -560,6 +599,30 @@ int tpmgo_cart_create(int64_t nx, int64_t ny, double hx, double hy, int64_t nz,
         L.sh[T] = w2 * ge_e * ps[T];
         L.sh[nc + T] = w2 * ge_n * ps[nc + T];
       }
+      // assemble_hatted, dense components (discretization.hpp:122-140, 196-203)
+      if (cm >= 1) {
+        L.ard.resize((nz + 1) * nc);
+        for (Index k = 0; k <= nz; ++k)
+          for (Index T = 0; T < nc; ++T)
+            L.ard[k * nc + T] = ((w2 * area) * fdiff[k]) * Da[k * nc + T];
+      }
+      if (cm == 2) {
+        L.bd.resize(nz * nc);
+        L.sd.resize(nz * 2 * nc);
+        for (Index k = 0; k < nz; ++k)
+          for (Index T = 0; T < nc; ++T) {
+            L.bd[k * nc + T] = area * (vol[k] * Db[k * nc + T]);
+            L.sd[k * 2 * nc + T] = ((w2 * (z[k + 1] - z[k])) * ge_e) * Ds[k * 2 * nc + T];
+            L.sd[k * 2 * nc + nc + T] =
+                ((w2 * (z[k + 1] - z[k])) * ge_n) * Ds[k * 2 * nc + nc + T];
+          }
+        if (!Dx.empty()) {
+          L.xid.resize((nz + 1) * nc);
+          for (Index k = 0; k <= nz; ++k)
+            for (Index T = 0; T < nc; ++T)
+              L.xid[k * nc + T] = ((w2 * area) * fadv[k]) * Dx[k * nc + T];
+        }
+      }
       if (l == 0) break;
       // restrict_profiles (factorised), multigrid.hpp:158-201 / :107-151.
       const Index ncx = cx / 2, ncy = cy / 2, ncc = ncx * ncy;
@@ -594,12 +657,75 @@ int tpmgo_cart_create(int64_t nx, int64_t ny, double hx, double hy, int64_t nz,
               (ps[nc + (2 * J + 1) * cx + 2 * I] + ps[nc + (2 * J + 1) * cx + 2 * I + 1]) / 2.0;
         }
       pb.swap(qb); pa.swap(qa); px.swap(qx); ps.swap(qs);
+      // restrict_profiles, dense rows (multigrid.hpp:107-151): the same means per level k
+      auto cell_rows = [&](std::vector<double>& D, Index rows) {
+        std::vector<double> q(rows * ncc);
+        for (Index k = 0; k < rows; ++k)
+          for (Index Tc = 0; Tc < ncc; ++Tc) {
+            const Index* chh = C.children.data() + Tc * 4;
+            double acc = 0.0, wsum = 0.0;
+            for (int j = 0; j < 4; ++j) {
+              acc += wf * D[k * nc + chh[j]];
+              wsum += wf;
+            }
+            q[k * ncc + Tc] = acc / wsum;
+          }
+        D.swap(q);
+      };
+      if (cm >= 1) cell_rows(Da, nz + 1);
+      if (cm == 2) {
+        cell_rows(Db, nz);
+        if (!Dx.empty()) cell_rows(Dx, nz + 1);
+        std::vector<double> q(nz * 2 * ncc);
+        for (Index k = 0; k < nz; ++k)
+          for (Index J = 0; J < ncy; ++J)
+            for (Index I = 0; I < ncx; ++I) {
+              const double* d = Ds.data() + k * 2 * nc;
+              const Index Tc = J * ncx + I;
+              q[k * 2 * ncc + Tc] = (d[(2 * J) * cx + 2 * I + 1] + d[(2 * J + 1) * cx + 2 * I + 1]) / 2.0;
+              q[k * 2 * ncc + ncc + Tc] =
+                  (d[nc + (2 * J + 1) * cx + 2 * I] + d[nc + (2 * J + 1) * cx + 2 * I + 1]) / 2.0;
+            }
+        Ds.swap(q);
+      }
       cx = ncx; cy = ncy;
       chx *= 2.0; chy *= 2.0;
     }
     finalize_nu(h, nu_pre, nu_post);
     *out = H;
   });
+}
+}  // namespace
+
+int tpmgo_cart_create(int64_t nx, int64_t ny, double hx, double hy, int64_t nz,
+                      const double* z, const double* beta_r, const double* alpha_s_r,
+                      const double* alpha_r_r, const double* xi_r_r, const double* beta_s,
+                      const double* alpha_r_s, const double* xi_r_s, const double* alpha_s_s,
+                      double omega, double relax, int prolongation, int restriction, int nu_pre,
+                      int nu_post, int depth, int threads, tpmgo_hier* out) {
+  return cart_create_impl(0, nullptr, nullptr, nullptr, nullptr, nx, ny, hx, hy, nz, z, beta_r,
+                          alpha_s_r, alpha_r_r, xi_r_r, beta_s, alpha_r_s, xi_r_s, alpha_s_s,
+                          omega, relax, prolongation, restriction, nu_pre, nu_post, depth,
+                          threads, out);
+}
+
+int tpmgo_cart_create_dense(int mode, const double* beta, const double* alpha_s,
+                            const double* alpha_r, const double* xi_r, int64_t nx, int64_t ny,
+                            double hx, double hy, int64_t nz, const double* z,
+                            const double* beta_r, const double* alpha_s_r,
+                            const double* alpha_r_r, const double* xi_r_r, const double* beta_s,
+                            const double* alpha_r_s, const double* xi_r_s,
+                            const double* alpha_s_s, double omega, double relax,
+                            int prolongation, int restriction, int nu_pre, int nu_post,
+                            int depth, int threads, tpmgo_hier* out) {
+  if (mode != 1 && mode != 2) {
+    g_last_error = "mode must be 1 (partial) or 2 (full)";
+    return E_CONFIG;
+  }
+  return cart_create_impl(mode, beta, alpha_s, alpha_r, xi_r, nx, ny, hx, hy, nz, z, beta_r,
+                          alpha_s_r, alpha_r_r, xi_r_r, beta_s, alpha_r_s, xi_r_s, alpha_s_s,
+                          omega, relax, prolongation, restriction, nu_pre, nu_post, depth,
+                          threads, out);
 }
 
 int tpmgo_generic_create(int n_levels, int64_t nz, int nnb, int nchild, const int64_t* ncells,

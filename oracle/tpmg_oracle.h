@@ -44,6 +44,20 @@ int tpmgo_cart_create(int64_t nx, int64_t ny, double hx, double hy, int64_t nz,
                       double omega, double relax, int prolongation, int restriction, int nu_pre,
                       int nu_post, int depth, int threads, tpmgo_hier* out);
 
+/* Partial (mode 1: dense alpha_r, MixedProfileSet) or full (mode 2: ProfileSet; the factorised
+ * pointers may be NULL) coefficients on the same Cartesian problem.  Dense inputs in the
+ * reference's Matrix order (k fastest): beta nz x ncells, alpha_s nz x 2 ncells (east, north),
+ * alpha_r / xi_r (nz+1) x ncells (xi_r may be NULL). */
+int tpmgo_cart_create_dense(int mode, const double* beta, const double* alpha_s,
+                            const double* alpha_r, const double* xi_r, int64_t nx, int64_t ny,
+                            double hx, double hy, int64_t nz, const double* z,
+                            const double* beta_r, const double* alpha_s_r,
+                            const double* alpha_r_r, const double* xi_r_r, const double* beta_s,
+                            const double* alpha_r_s, const double* xi_r_s,
+                            const double* alpha_s_s, double omega, double relax,
+                            int prolongation, int restriction, int nu_pre, int nu_post,
+                            int depth, int threads, tpmgo_hier* out);
+
 /* Generic tables (one entry per level, coarsest first).  Per level l:
  * ncells[l], nedges[l]; nbr[l] / cedge[l]: ncells*nnb Index, entry T*nnb+d
  * (= Index3X neighbors(d,T) column-major); children[l] for l>=1: ncells[l-1]*nchild,

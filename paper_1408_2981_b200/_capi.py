@@ -56,6 +56,11 @@ SIGNATURES = {
     "tpmg_bicgstab": (C.c_int, [_VP, _VP, _VP, C.c_double, C.c_int, C.c_int, _D, C.POINTER(C.c_int),
                                 C.POINTER(C.c_int)]),
     "tpmg_solver_counts": (C.c_int, [_VP, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "tpmg_hier_create_partial": (C.c_int, [_VP, C.c_void_p, C.c_void_p, _D, C.c_double, C.c_void_p,
+                                           C.POINTER(_VP)]),
+    "tpmg_hier_create_full": (C.c_int, [_VP, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,
+                                        C.POINTER(_VP)]),
+    "tpmg_hier_coef_mode": (C.c_int, [_VP, C.POINTER(C.c_int)]),
     "tpmg_pcg_host": (C.c_int, [_VP, _D, _D, C.c_int, C.c_double, C.c_int, _D, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "tpmg_kernel_launch_count": (C.c_int, [_VP, C.POINTER(C.c_int64)]),
     "tpmg_set_use_graphs": (C.c_int, [_VP, C.c_int]),
@@ -76,6 +81,10 @@ class GridDesc(C.Structure):
 class FactorizedProfiles(C.Structure):
     _fields_ = [(n, _D) for n in ("beta_r", "alpha_s_r", "alpha_r_r", "xi_r_r", "beta_s",
                                   "alpha_r_s", "xi_r_s", "alpha_s_s")]
+
+
+class FullProfiles(C.Structure):  # tpmg_full_profiles
+    _fields_ = [(n, _D) for n in ("beta", "alpha_s", "alpha_r", "xi_r")]
 
 
 class MGConfig(C.Structure):

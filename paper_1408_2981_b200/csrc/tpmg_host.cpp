@@ -132,6 +132,9 @@ struct Level {
   // host copies of the hatted horizontal factors (tile local)
   std::vector<double> bh, ah, xh, sh;  // sh: 2*plane (east, north)
   DevBuf d_bh, d_ah, d_xh, d_sw, d_se, d_ss, d_sn;
+  // dense hatted components of the partial / full coefficient modes, [k][y][x]
+  int cm = tpmg::CM_FACT;
+  DevBuf d_ard, d_bd, d_xid, d_swd, d_sed, d_ssd, d_snd;
   DevBuf u, t, f;              // V-cycle work: home iterate, ping-pong partner, rhs
   DevBuf send, recv;           // multi-GPU face buffers [W|E|S|N]
   LevelCoef coef(int nz) const {
@@ -139,6 +142,9 @@ struct Level {
     c.nx = nx; c.ny = ny; c.nz = nz; c.plane = plane;
     c.bh = d_bh.p; c.ah = d_ah.p; c.xh = d_xh.p;
     c.sw = d_sw.p; c.se = d_se.p; c.ss = d_ss.p; c.sn = d_sn.p;
+    c.cm = cm;
+    c.ard = d_ard.p; c.bd = d_bd.p; c.xid = d_xid.p;
+    c.swd = d_swd.p; c.sed = d_sed.p; c.ssd = d_ssd.p; c.snd = d_snd.p;
     return c;
   }
 };
@@ -149,6 +155,7 @@ struct tpmg_hierarchy_s {
   tpmg_context ctx = nullptr;
   int nz = 0;
   bool xi = false;
+  int cm = 0;  // coefficient mode (tpmg::CoefMode)
   double relax = 1.0;
   int prolongation = 0, restriction = 0;
   std::vector<int> nu_pre, nu_post;
@@ -645,11 +652,19 @@ int tpmg_plan_decomposition(int64_t nx, int64_t ny, int px, int py, int rank, in
   });
 }
 
-int tpmg_hier_create(tpmg_context ctx, const tpmg_grid_desc* g,
-                     const tpmg_factorized_profiles* p, double omega, const tpmg_mg_config* cfg,
-                     tpmg_hierarchy* out) {
+namespace {
+// build_hierarchy_coefficients (multigrid.hpp:242-272) for the three profile kinds of the
+// reference's ProfileVariant (multigrid.hpp:102-103): factorised `p`; partial = `p` with
+// alpha_r dense (`ar`, MixedProfileSet); full `fp` (ProfileSet).  Dense profiles are restricted
+// level by level exactly like the factorised horizontal scalars (restrict_profiles,
+// multigrid.hpp:146-201) and assembled per level (assemble_hatted, discretization.hpp:104-141,
+// 187-204) into [k][y][x] device arrays.
+int hier_create_impl(tpmg_context ctx, const tpmg_grid_desc* g, const tpmg_factorized_profiles* p,
+                     const tpmg_full_profiles* fp, const double* ar, double omega,
+                     const tpmg_mg_config* cfg, tpmg_hierarchy* out) {
   return guard(ctx, [&] {
-    if (!ctx || !g || !p || !cfg || !out) throw Error(TPMG_E_CONFIG, "null argument");
+    if (!ctx || !g || !(p || fp) || !cfg || !out) throw Error(TPMG_E_CONFIG, "null argument");
+    const int cm = fp ? tpmg::CM_FULL : (ar ? tpmg::CM_PARTIAL : tpmg::CM_FACT);
     CUDA_CHECK(cudaSetDevice(ctx->device));
     const int64_t NX = g->nx, NY = g->ny, nz = g->nz;
     if (NX < 1 || NY < 1 || nz < 1) throw Error(TPMG_E_CONFIG, "grid dimensions must be positive");
@@ -668,14 +683,25 @@ int tpmg_hier_create(tpmg_context ctx, const tpmg_grid_desc* g,
       if (!(g->z_faces[k + 1] > g->z_faces[k]))
         throw Error(TPMG_E_CONFIG, "vertical faces must increase");
     const int64_t ncf = NX * NY;
-    check_finite(p->beta_r, nz, "beta_r");
-    check_finite(p->alpha_s_r, nz, "alpha_s_r");
-    check_finite(p->alpha_r_r, nz + 1, "alpha_r_r");
-    if (p->xi_r_r) check_finite(p->xi_r_r, nz + 1, "xi_r_r");
-    check_finite(p->beta_s, ncf, "beta_s");
-    check_finite(p->alpha_r_s, ncf, "alpha_r_s");
-    if (p->xi_r_s) check_finite(p->xi_r_s, ncf, "xi_r_s");
-    check_finite(p->alpha_s_s, 2 * ncf, "alpha_s_s");
+    if (p) {
+      check_finite(p->beta_r, nz, "beta_r");
+      check_finite(p->alpha_s_r, nz, "alpha_s_r");
+      check_finite(p->alpha_r_r, nz + 1, "alpha_r_r");
+      if (p->xi_r_r) check_finite(p->xi_r_r, nz + 1, "xi_r_r");
+      check_finite(p->beta_s, ncf, "beta_s");
+      check_finite(p->alpha_r_s, ncf, "alpha_r_s");
+      if (p->xi_r_s) check_finite(p->xi_r_s, ncf, "xi_r_s");
+      check_finite(p->alpha_s_s, 2 * ncf, "alpha_s_s");
+    }
+    if (ar) check_finite(ar, (nz + 1) * ncf, "alpha_r (full)");
+    if (fp) {
+      if (!fp->beta || !fp->alpha_s || !fp->alpha_r)
+        throw Error(TPMG_E_CONFIG, "full profiles: beta, alpha_s and alpha_r are required");
+      check_finite(fp->beta, nz * ncf, "beta");
+      check_finite(fp->alpha_s, nz * 2 * ncf, "alpha_s");
+      check_finite(fp->alpha_r, (nz + 1) * ncf, "alpha_r");
+      if (fp->xi_r) check_finite(fp->xi_r, (nz + 1) * ncf, "xi_r");
+    }
 
     const int levels = plan_levels(NX, NY, ctx->px, ctx->py, cfg->depth,
                                    cfg->prolongation == TPMG_PROLONG_LINEAR ||
@@ -684,7 +710,8 @@ int tpmg_hier_create(tpmg_context ctx, const tpmg_grid_desc* g,
     auto h = std::make_unique<tpmg_hierarchy_s>();
     h->ctx = ctx;
     h->nz = (int)nz;
-    h->xi = p->xi_r_r != nullptr && p->xi_r_s != nullptr;
+    h->xi = fp ? fp->xi_r != nullptr : (p->xi_r_r != nullptr && p->xi_r_s != nullptr);
+    h->cm = cm;
     h->relax = cfg->relax;
     h->prolongation = cfg->prolongation;
     h->restriction = cfg->restriction;
@@ -696,23 +723,49 @@ int tpmg_hier_create(tpmg_context ctx, const tpmg_grid_desc* g,
 
     // vertical hatted vectors (discretization.hpp:165-181, flat: volumes dz_k, r_k^2 -> 1)
     const double* z = g->z_faces;
-    h->bv.resize(nz); h->sv.resize(nz); h->av.assign(nz + 1, 0.0); h->xv.assign(nz + 1, 0.0);
-    for (int64_t k = 0; k < nz; ++k) {
-      h->bv[k] = (z[k + 1] - z[k]) * p->beta_r[k];
-      h->sv[k] = (z[k + 1] - z[k]) * p->alpha_s_r[k];
+    // face factors (discretization.hpp:72-87, flat: r_k^2 -> 1), zero on the boundary faces
+    std::vector<double> fdiff(nz + 1, 0.0), fadv(nz + 1, 0.0);
+    for (int64_t k = 1; k < nz; ++k) {
+      fdiff[k] = 2.0 / (z[k + 1] - z[k - 1]);
+      fadv[k] = (z[k + 1] - z[k]) / (z[k + 1] - z[k - 1]);
     }
-    for (int64_t k = 0; k <= nz; ++k) {
-      const double fd = (k >= 1 && k < nz) ? 2.0 / (z[k + 1] - z[k - 1]) : 0.0;
-      const double fa = (k >= 1 && k < nz) ? (z[k + 1] - z[k]) / (z[k + 1] - z[k - 1]) : 0.0;
-      h->av[k] = fd * p->alpha_r_r[k];
-      if (h->xi) h->xv[k] = fa * p->xi_r_r[k];
+    h->bv.assign(nz, 0.0); h->sv.assign(nz, 0.0); h->av.assign(nz + 1, 0.0); h->xv.assign(nz + 1, 0.0);
+    if (p) {
+      for (int64_t k = 0; k < nz; ++k) {
+        h->bv[k] = (z[k + 1] - z[k]) * p->beta_r[k];
+        h->sv[k] = (z[k + 1] - z[k]) * p->alpha_s_r[k];
+      }
+      for (int64_t k = 0; k <= nz; ++k) {
+        const double fd = (k >= 1 && k < nz) ? 2.0 / (z[k + 1] - z[k - 1]) : 0.0;
+        const double fa = (k >= 1 && k < nz) ? (z[k + 1] - z[k]) / (z[k + 1] - z[k - 1]) : 0.0;
+        h->av[k] = fd * p->alpha_r_r[k];
+        if (h->xi) h->xv[k] = fa * p->xi_r_r[k];
+      }
     }
     const double w2 = omega * omega;
 
     // horizontal profiles on the current (global) level, restricted level by level
-    std::vector<double> pb(p->beta_s, p->beta_s + ncf), pa(p->alpha_r_s, p->alpha_r_s + ncf);
-    std::vector<double> px(ncf, 0.0), ps(p->alpha_s_s, p->alpha_s_s + 2 * ncf);
-    if (h->xi) px.assign(p->xi_r_s, p->xi_r_s + ncf);
+    std::vector<double> pb(ncf, 0.0), pa(ncf, 0.0), px(ncf, 0.0), ps(2 * ncf, 0.0);
+    if (p) {
+      pb.assign(p->beta_s, p->beta_s + ncf);
+      pa.assign(p->alpha_r_s, p->alpha_r_s + ncf);
+      ps.assign(p->alpha_s_s, p->alpha_s_s + 2 * ncf);
+      if (h->xi) px.assign(p->xi_r_s, p->xi_r_s + ncf);
+    }
+    // dense profiles, [k][global cell] (input: the reference's column-major, k fastest)
+    std::vector<double> Da, Db, Dx, Ds;
+    auto to_kc = [&](const double* in, int64_t rows, int64_t cols, std::vector<double>& outv) {
+      outv.resize(rows * cols);
+      for (int64_t c = 0; c < cols; ++c)
+        for (int64_t k = 0; k < rows; ++k) outv[k * cols + c] = in[c * rows + k];
+    };
+    if (ar) to_kc(ar, nz + 1, ncf, Da);
+    if (fp) {
+      to_kc(fp->alpha_r, nz + 1, ncf, Da);
+      to_kc(fp->beta, nz, ncf, Db);
+      to_kc(fp->alpha_s, nz, 2 * ncf, Ds);
+      if (fp->xi_r) to_kc(fp->xi_r, nz + 1, ncf, Dx);
+    }
     int64_t gx = NX, gy = NY;
     double hx = g->hx, hy = g->hy;
     for (int l = levels - 1; l >= 0; --l) {
@@ -749,7 +802,86 @@ int tpmg_hier_create(tpmg_context ctx, const tpmg_grid_desc* g,
       L.d_se.upload(se.data(), L.plane);
       L.d_ss.upload(ss.data(), L.plane);
       L.d_sn.upload(sn.data(), L.plane);
+      L.cm = cm;
+      if (cm != tpmg::CM_FACT) {
+        // assemble_hatted, dense components (discretization.hpp:122-140, 196-203):
+        // alpha_r hat = ((w2 |T|) f_k) alpha_r; beta hat = |T| (dz_k beta);
+        // alpha_s hat = ((w2 dz_k) g_e) alpha_s; xi_r hat = ((w2 |T|) fadv_k) xi_r
+        const int64_t P = L.plane;
+        std::vector<double> v((nz + 1) * P);
+        auto tile = [&](int64_t rows, auto&& val, DevBuf& dst) {
+          for (int64_t k = 0; k < rows; ++k)
+            for (int j = 0; j < L.ny; ++j)
+              for (int i = 0; i < L.nx; ++i) {
+                const int64_t gi = L.x0 + i, gj = L.y0 + j;
+                v[k * P + (int64_t)j * L.nx + i] = val(k, gi, gj);
+              }
+          dst.upload(v.data(), rows * P);
+        };
+        tile(nz + 1, [&](int64_t k, int64_t gi, int64_t gj) {
+          return ((w2 * area) * fdiff[k]) * Da[k * gnc + gj * gx + gi];
+        }, L.d_ard);
+        if (cm == tpmg::CM_FULL) {
+          tile(nz, [&](int64_t k, int64_t gi, int64_t gj) {
+            return area * ((z[k + 1] - z[k]) * Db[k * gnc + gj * gx + gi]);
+          }, L.d_bd);
+          if (h->xi)
+            tile(nz + 1, [&](int64_t k, int64_t gi, int64_t gj) {
+              return ((w2 * area) * fadv[k]) * Dx[k * gnc + gj * gx + gi];
+            }, L.d_xid);
+          auto edge = [&](int64_t k, int64_t e, double ge) {
+            return ((w2 * (z[k + 1] - z[k])) * ge) * Ds[k * 2 * gnc + e];
+          };
+          tile(nz, [&](int64_t k, int64_t gi, int64_t gj) {
+            return edge(k, gj * gx + (gi + gx - 1) % gx, ge_e);  // east edge of the W cell
+          }, L.d_swd);
+          tile(nz, [&](int64_t k, int64_t gi, int64_t gj) { return edge(k, gj * gx + gi, ge_e); },
+               L.d_sed);
+          tile(nz, [&](int64_t k, int64_t gi, int64_t gj) {
+            return edge(k, gnc + ((gj + gy - 1) % gy) * gx + gi, ge_n);  // north of the S cell
+          }, L.d_ssd);
+          tile(nz, [&](int64_t k, int64_t gi, int64_t gj) {
+            return edge(k, gnc + gj * gx + gi, ge_n);
+          }, L.d_snd);
+        }
+      }
       if (l == 0) break;
+      if (cm != tpmg::CM_FACT) {
+        // restrict_profiles, dense rows (multigrid.hpp:107-151, 146-156, 193-201)
+        const int64_t cx = gx / 2, cy = gy / 2, cnc = cx * cy;
+        const double wf = hx * hy;
+        auto cell_rows = [&](std::vector<double>& D, int64_t rows) {
+          std::vector<double> q(rows * cnc);
+          for (int64_t k = 0; k < rows; ++k)
+            for (int64_t J = 0; J < cy; ++J)
+              for (int64_t I = 0; I < cx; ++I) {
+                const int64_t c0 = (2 * J) * gx + 2 * I, c1 = c0 + 1, c2 = c0 + gx, c3 = c2 + 1;
+                const double* d = D.data() + k * gnc;
+                double acc = 0.0, ws = 0.0;
+                acc += wf * d[c0]; ws += wf;
+                acc += wf * d[c1]; ws += wf;
+                acc += wf * d[c2]; ws += wf;
+                acc += wf * d[c3]; ws += wf;
+                q[k * cnc + J * cx + I] = acc / ws;
+              }
+          D.swap(q);
+        };
+        cell_rows(Da, nz + 1);
+        if (cm == tpmg::CM_FULL) {
+          cell_rows(Db, nz);
+          if (h->xi) cell_rows(Dx, nz + 1);
+          std::vector<double> q(nz * 2 * cnc);
+          for (int64_t k = 0; k < nz; ++k)
+            for (int64_t J = 0; J < cy; ++J)
+              for (int64_t I = 0; I < cx; ++I) {
+                const double* d = Ds.data() + k * 2 * gnc;
+                const int64_t c0 = (2 * J) * gx + 2 * I, c1 = c0 + 1, c2 = c0 + gx, c3 = c2 + 1;
+                q[k * 2 * cnc + J * cx + I] = (d[c1] + d[c3]) / 2.0;
+                q[k * 2 * cnc + cnc + J * cx + I] = (d[gnc + c2] + d[gnc + c3]) / 2.0;
+              }
+          Ds.swap(q);
+        }
+      }
       // restrict_profiles (factorised), multigrid.hpp:158-201: area-weighted mean of the 4
       // children (:108-124), mean of the 2 co-linear child edges (:135-143)
       const int64_t cx = gx / 2, cy = gy / 2, cnc = cx * cy;
@@ -830,6 +962,31 @@ int tpmg_hier_create(tpmg_context ctx, const tpmg_grid_desc* g,
     }
     *out = h.release();
   });
+}
+}  // namespace
+
+int tpmg_hier_create(tpmg_context ctx, const tpmg_grid_desc* g,
+                     const tpmg_factorized_profiles* p, double omega, const tpmg_mg_config* cfg,
+                     tpmg_hierarchy* out) {
+  if (!p) return hier_create_impl(ctx, nullptr, nullptr, nullptr, nullptr, omega, cfg, out);
+  return hier_create_impl(ctx, g, p, nullptr, nullptr, omega, cfg, out);
+}
+
+int tpmg_hier_create_partial(tpmg_context ctx, const tpmg_grid_desc* g,
+                             const tpmg_factorized_profiles* p, const double* alpha_r,
+                             double omega, const tpmg_mg_config* cfg, tpmg_hierarchy* out) {
+  if (!p || !alpha_r) return hier_create_impl(ctx, nullptr, nullptr, nullptr, nullptr, omega, cfg, out);
+  return hier_create_impl(ctx, g, p, nullptr, alpha_r, omega, cfg, out);
+}
+
+int tpmg_hier_create_full(tpmg_context ctx, const tpmg_grid_desc* g, const tpmg_full_profiles* fp,
+                          double omega, const tpmg_mg_config* cfg, tpmg_hierarchy* out) {
+  if (!fp) return hier_create_impl(ctx, nullptr, nullptr, nullptr, nullptr, omega, cfg, out);
+  return hier_create_impl(ctx, g, nullptr, fp, nullptr, omega, cfg, out);
+}
+
+int tpmg_hier_coef_mode(tpmg_hierarchy h, int* mode) {
+  return guard(h ? h->ctx : nullptr, [&] { *mode = h->cm; });
 }
 
 int tpmg_hier_destroy(tpmg_hierarchy h) {

@@ -21,6 +21,11 @@ struct VertCoef {      // HattedComponent::vert of beta, alpha_s, alpha_r, xi_r
   const double* xv;    // nz+1 (only read when the level has advection)
 };
 
+// Coefficient storage of a level (HattedComponent, discretization.hpp:32-48): factorised
+// (TPMG-tensor-product: vertical x horizontal factors), partial (alpha_r hat dense, the rest
+// factorised: MixedProfileSet, profiles.hpp:225-233), full (every component dense: ProfileSet).
+enum CoefMode { CM_FACT = 0, CM_PARTIAL = 1, CM_FULL = 2 };
+
 struct LevelCoef {     // HattedComponent::horiz, per column of the local tile
   int nx, ny, nz;
   int64_t plane;       // nx*ny
@@ -31,6 +36,15 @@ struct LevelCoef {     // HattedComponent::horiz, per column of the local tile
   const double* se;
   const double* ss;
   const double* sn;
+  int cm = CM_FACT;
+  // dense components, [k][y][x] like the fields (HattedComponent::dense):
+  const double* ard = nullptr;  // alpha_r hat, nz+1 planes (partial, full)
+  const double* bd = nullptr;   // beta hat, nz planes (full)
+  const double* xid = nullptr;  // xi_r hat, nz+1 planes (full, with advection)
+  const double* swd = nullptr;  // alpha_s hat of the W / E / S / N edge of each cell (full)
+  const double* sed = nullptr;
+  const double* ssd = nullptr;
+  const double* snd = nullptr;
 };
 
 // Where the neighbour values across each tile face live.  For direction d

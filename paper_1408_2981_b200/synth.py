@@ -199,6 +199,10 @@ class Problem:
     name: str = ""
     xi_r_r: np.ndarray | None = None  # vertical advection (nz+1), None = xi == 0
     xi_r_s: np.ndarray | None = None  # (nx*ny)
+    # coefficient storage: "factorized" (the profiles above), "partial" (dense["alpha_r"]
+    # replaces alpha_r: MixedProfileSet) or "full" (dense ProfileSet, see dense_profiles)
+    coef: str = "factorized"
+    dense: dict | None = None
 
     @property
     def n_dof(self) -> int:
@@ -220,6 +224,36 @@ def edge_profile(h: np.ndarray, nx: int, ny: int) -> np.ndarray:
     east = 0.5 * (hh + np.roll(hh, -1, axis=1))
     north = 0.5 * (hh + np.roll(hh, -1, axis=0))
     return np.concatenate([east.reshape(-1), north.reshape(-1)])
+
+
+def dense_profiles(P: Problem, eps: float = 0.1, seed: int = 7) -> dict:
+    """A genuinely non-separable ProfileSet (profiles.hpp:182-192) near P's factorised one:
+    each dense entry is the outer product of P's vertical and horizontal factors times
+    (1 + eps * U[-1, 1)) drawn per (level, cell/edge).  Arrays in the reference's Matrix order
+    (k fastest): shape (n_cells or n_edges, rows), C-contiguous."""
+    rng = np.random.default_rng(seed)
+    nc = P.nx * P.ny
+
+    def outer(vert, horiz):
+        d = np.outer(np.asarray(horiz, dtype=np.float64), np.asarray(vert, dtype=np.float64))
+        return np.ascontiguousarray(d * (1.0 + eps * rng.uniform(-1.0, 1.0, d.shape)))
+
+    out = dict(beta=outer(P.beta_r, P.beta_s), alpha_s=outer(P.alpha_s_r, P.alpha_s_s),
+               alpha_r=outer(P.alpha_r_r, P.alpha_r_s), xi_r=None)
+    if P.xi_r_r is not None:
+        out["xi_r"] = outer(P.xi_r_r, P.xi_r_s)
+    assert out["beta"].shape == (nc, P.nz) and out["alpha_s"].shape == (2 * nc, P.nz)
+    return out
+
+
+def with_coefficients(P: Problem, coef: str, eps: float = 0.1, seed: int = 7) -> Problem:
+    """Copy of P with partial ("partial": dense alpha_r) or full ("full") coefficients."""
+    assert coef in ("factorized", "partial", "full")
+    Q = dataclasses.replace(P)
+    Q.coef = coef
+    Q.dense = None if coef == "factorized" else dense_profiles(P, eps, seed)
+    Q.name = f"{P.name}-{coef}"
+    return Q
 
 
 def make_problem(nx: int, ny: int, nz: int, *, omega2: float, lambda2: float,

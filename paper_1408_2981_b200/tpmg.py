@@ -18,7 +18,7 @@ import time
 import numpy as np
 
 from . import _capi
-from ._capi import ContextParams, FactorizedProfiles, GridDesc, MGConfig
+from ._capi import ContextParams, FactorizedProfiles, FullProfiles, GridDesc, MGConfig
 
 K_FASTEST, X_FASTEST = 0, 1
 (K_APPLY, K_JACOBI, K_JACOBI_ZERO, K_RESID_RESTRICT, K_PROLONG_ADD, K_RESTRICT, K_RESIDUAL,
@@ -234,8 +234,26 @@ class Hierarchy:
                        kw["nu_pre"], kw["nu_post"], kw["depth"])
         h = C.c_void_p()
         self._h = None
-        ctx._check(self.lib.tpmg_hier_create(ctx._h, C.byref(grid), C.byref(prof),
-                                             C.c_double(P.omega), C.byref(cfg), C.byref(h)))
+        coef = getattr(P, "coef", "factorized")
+        if coef == "factorized":
+            ctx._check(self.lib.tpmg_hier_create(ctx._h, C.byref(grid), C.byref(prof),
+                                                 C.c_double(P.omega), C.byref(cfg), C.byref(h)))
+        elif coef == "partial":
+            ar = np.ascontiguousarray(P.dense["alpha_r"], dtype=np.float64)
+            self._keep.append(ar)
+            ctx._check(self.lib.tpmg_hier_create_partial(ctx._h, C.byref(grid), C.byref(prof),
+                                                         _p(ar), C.c_double(P.omega),
+                                                         C.byref(cfg), C.byref(h)))
+        elif coef == "full":
+            d = {k: (None if v is None else np.ascontiguousarray(v, dtype=np.float64))
+                 for k, v in P.dense.items()}
+            self._keep += [v for v in d.values() if v is not None]
+            fp = FullProfiles(_p(d["beta"]), _p(d["alpha_s"]), _p(d["alpha_r"]), _p(d["xi_r"]))
+            ctx._check(self.lib.tpmg_hier_create_full(ctx._h, C.byref(grid), C.byref(fp),
+                                                      C.c_double(P.omega), C.byref(cfg),
+                                                      C.byref(h)))
+        else:
+            raise config_error(f"unknown coefficient storage {coef!r}")
         self._h = h
         ctx._live_children += 1
         self._keep = None

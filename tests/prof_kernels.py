@@ -18,7 +18,10 @@ def main():
     ctx = tpmg.Context()
     over = {k.lower(): int(os.environ["TPMG_" + k]) for k in ("NX", "NY", "DEPTH")
             if "TPMG_" + k in os.environ}
-    h = tpmg.Hierarchy(ctx, synth.baseline_config(cfg, **over))
+    P = synth.baseline_config(cfg, **over)
+    if os.environ.get("TPMG_COEF", "factorized") != "factorized":
+        P = synth.with_coefficients(P, os.environ["TPMG_COEF"])
+    h = tpmg.Hierarchy(ctx, P)
     for n in names:
         ms = h.time_kernel(KERNELS[n], h.finest, reps=reps)
         print(f"{n}: {ms:.3f} ms", flush=True)

@@ -11,6 +11,8 @@ from paper_1408_2981_b200 import synth, tpmg  # noqa: E402
 
 def main():
     P = synth.baseline_config(int(os.environ.get("TPMG_CFG", "3")))
+    if os.environ.get("TPMG_COEF", "factorized") != "factorized":
+        P = synth.with_coefficients(P, os.environ["TPMG_COEF"])
     ctx = tpmg.Context()
     h = tpmg.Hierarchy(ctx, P)
     h.set_use_graphs(os.environ.get("TPMG_GRAPHS", "1") == "1")
