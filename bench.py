@@ -182,6 +182,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--max-iter", type=int, default=500)
+    ap.add_argument("--no-coef", action="store_true", help="skip the coefficient-storage comparison")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -308,6 +309,33 @@ def main():
     e5.synchronize()
     vcycle_ms = e4.elapsed_time(e5) / 5
 
+    # ---- coefficient storage trade-off (PAPER's TPMG(full) vs
+    # TPMG(partial) vs tensor-product): the same PCG solve with partial and full (dense) hatted
+    # coefficients, at BASELINE config 2's size so that the default run stays short -----------
+    coef_modes = None
+    if world == 1 and not args.no_coef:
+        P2 = synth.baseline_config(2)
+        coef_modes = {"workload": f"{P2.name}: PCG + V(1,1) to 1e-8, one warm and one timed solve",
+                      "coef_bytes_per_dof": {"factorized": 0, "partial": 8, "full": 48}}
+        f2 = P2.rhs()
+        for mode in ("factorized", "partial", "full"):
+            Q = P2 if mode == "factorized" else synth.with_coefficients(P2, mode)
+            h2 = tpmg.Hierarchy(ctx, Q)
+            ff2, x2 = h2.field().upload(f2), h2.field()
+            tpmg.pcg_solve(h2, ff2, x2, Q.tol, args.max_iter)  # warm (captures the graph)
+            torch.cuda.synchronize()
+            e6, e7 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e6.record(stream)
+            r6 = tpmg.pcg_solve(h2, ff2, x2, Q.tol, args.max_iter)
+            e7.record(stream)
+            e7.synchronize()
+            ms6 = e6.elapsed_time(e7)
+            coef_modes[mode] = {"ms_per_solve": ms6, "iterations": r6.iterations,
+                                "gdof_per_s": Q.n_dof * r6.iterations / (ms6 * 1e-3) / 1e9,
+                                "jacobi_ms": h2.time_kernel(tpmg.K_JACOBI, h2.finest, reps=10)}
+            del ff2, x2
+            h2.close()
+
     traffic = None
     prof_json = os.path.join(ROOT, "profiles", "jacobi_traffic.json")
     if os.path.exists(prof_json):
@@ -335,6 +363,7 @@ def main():
                      "traffic": traffic, "algorithmic_bytes": jac_bytes, "launch_ms": t_jac,
                      "peak_kind": peak_kind},
         "kernels": kernels,
+        "coef_modes": coef_modes,
         "e2e": {"value": e2e_value, "unit": "GDOF/s", "h2d_bytes_per_step": 8 * n_local,
                 "d2h_bytes_per_step": 8 * n_local, "ms_per_step": e2e_ms / args.steps},
         "clocks": clk.summary(),
