@@ -172,6 +172,24 @@ int tpmg_hier_create_full(tpmg_context ctx, const tpmg_grid_desc* grid,
                           const tpmg_full_profiles* profiles, double omega,
                           const tpmg_mg_config* cfg, tpmg_hierarchy* out);
 int tpmg_hier_coef_mode(tpmg_hierarchy h, int* mode);
+/* build_hierarchy_coefficients' result on an arbitrary (indirect) grid hierarchy, e.g. the
+ * reference's icosahedral GridHierarchy (geometry.hpp:41-91): per level (coarsest first)
+ * ncells / nedges, neighbour and edge tables ncells x nnb (entry T*nnb + j = the reference's
+ * Index3X neighbors(j, T) / cell_edges(j, T)), the child table of every level but the coarsest
+ * (entry Tc*nchild + j on the next coarser level's cell Tc = GridHierarchy::child_of), the
+ * prolongation's corner rule prol_d1/prol_d2 (-1 = centre child, multigrid.hpp:88-95), and the
+ * separable hatted coefficients (vertical bv, sv nz; av, xv nz+1; horizontal bh, ah, xh per cell
+ * and sh per edge, discretization.hpp:32-48).  One rank.  Fields of such a hierarchy are
+ * [k][cell] on the device; nx = ncells, ny = 1 in tpmg_hier_level_shape. */
+int tpmg_hier_create_generic(tpmg_context ctx, int n_levels, int nz, int nnb, int nchild,
+                             const int64_t* ncells, const int64_t* nedges,
+                             const int64_t* const* nbr, const int64_t* const* cedge,
+                             const int64_t* const* children, const int* prol_d1,
+                             const int* prol_d2, const double* bv, const double* sv,
+                             const double* av, const double* xv, const double* const* bh,
+                             const double* const* ah, const double* const* xh,
+                             const double* const* sh, double relax, int prolongation,
+                             int restriction, int nu_pre, int nu_post, tpmg_hierarchy* out);
 int tpmg_hier_destroy(tpmg_hierarchy h);
 int tpmg_hier_n_levels(tpmg_hierarchy h, int* n_levels);
 /* Local tile shape and global offset of `level` on this rank. */

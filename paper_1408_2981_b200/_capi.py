@@ -61,6 +61,15 @@ SIGNATURES = {
     "tpmg_hier_create_full": (C.c_int, [_VP, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,
                                         C.POINTER(_VP)]),
     "tpmg_hier_coef_mode": (C.c_int, [_VP, C.POINTER(C.c_int)]),
+    "tpmg_hier_create_generic": (C.c_int, [_VP, C.c_int, C.c_int, C.c_int, C.c_int,
+                                           C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                           C.POINTER(C.POINTER(C.c_int64)),
+                                           C.POINTER(C.POINTER(C.c_int64)),
+                                           C.POINTER(C.POINTER(C.c_int64)),
+                                           C.POINTER(C.c_int), C.POINTER(C.c_int), _D, _D, _D, _D,
+                                           C.POINTER(_D), C.POINTER(_D), C.POINTER(_D),
+                                           C.POINTER(_D), C.c_double, C.c_int, C.c_int, C.c_int,
+                                           C.c_int, C.POINTER(_VP)]),
     "tpmg_pcg_host": (C.c_int, [_VP, _D, _D, C.c_int, C.c_double, C.c_int, _D, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "tpmg_kernel_launch_count": (C.c_int, [_VP, C.POINTER(C.c_int64)]),
     "tpmg_set_use_graphs": (C.c_int, [_VP, C.c_int]),

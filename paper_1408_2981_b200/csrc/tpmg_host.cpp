@@ -108,21 +108,23 @@ struct tpmg_context_s {
 
 namespace {
 
-struct DevBuf {
-  double* p = nullptr;
+template <typename T>
+struct DevBufT {
+  T* p = nullptr;
   size_t n = 0;
   void alloc(size_t count) {
     n = count;
-    CUDA_CHECK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(double)));
+    CUDA_CHECK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
   }
-  void upload(const double* h, size_t count) {
+  void upload(const T* h, size_t count) {
     alloc(count);
-    CUDA_CHECK(cudaMemcpy(p, h, count * sizeof(double), cudaMemcpyHostToDevice));
+    CUDA_CHECK(cudaMemcpy(p, h, count * sizeof(T), cudaMemcpyHostToDevice));
   }
-  ~DevBuf() {
+  ~DevBufT() {
     if (p) cudaFree(p);
   }
 };
+using DevBuf = DevBufT<double>;
 
 struct Level {
   int nx = 0, ny = 0;          // local tile
@@ -135,6 +137,11 @@ struct Level {
   // dense hatted components of the partial / full coefficient modes, [k][y][x]
   int cm = tpmg::CM_FACT;
   DevBuf d_ard, d_bd, d_xid, d_swd, d_sed, d_ssd, d_snd;
+  // indirect levels (tpmg_hier_create_generic): neighbour / edge tables, per-edge alpha_s hat,
+  // and (coarse levels) the child table on the next finer level
+  int nnb = 0;
+  DevBufT<int> d_nbr, d_cedge, d_children;
+  DevBuf d_shg;
   DevBuf u, t, f;              // V-cycle work: home iterate, ping-pong partner, rhs
   DevBuf send, recv;           // multi-GPU face buffers [W|E|S|N]
   LevelCoef coef(int nz) const {
@@ -145,6 +152,7 @@ struct Level {
     c.cm = cm;
     c.ard = d_ard.p; c.bd = d_bd.p; c.xid = d_xid.p;
     c.swd = d_swd.p; c.sed = d_sed.p; c.ssd = d_ssd.p; c.snd = d_snd.p;
+    c.nnb = nnb; c.nbr = d_nbr.p; c.cedge = d_cedge.p; c.shg = d_shg.p;
     return c;
   }
 };
@@ -156,6 +164,8 @@ struct tpmg_hierarchy_s {
   int nz = 0;
   bool xi = false;
   int cm = 0;  // coefficient mode (tpmg::CoefMode)
+  bool generic = false;     // indirect levels (tpmg_hier_create_generic)
+  tpmg::GenRule rule{};
   double relax = 1.0;
   int prolongation = 0, restriction = 0;
   std::vector<int> nu_pre, nu_post;
@@ -343,10 +353,17 @@ void sweep(tpmg_hierarchy h, int l, const double* u_in, const double* f, double*
 }
 
 // fine level lf -> coarse lf-1: coarse = R (f - A u).  `scratch` is a free fine-level buffer.
+void restrict_plain(tpmg_hierarchy h, int lf, const double* fine, double* coarse);
+
 void resid_restrict(tpmg_hierarchy h, int lf, const double* u, const double* f, double* coarse,
                     double* scratch) {
   Level& F = h->lv[lf];
   Level& C = h->lv[lf - 1];
+  if (h->generic) {
+    apply_level(h, lf, tpmg::APPLY_RESID, u, f, scratch);
+    restrict_plain(h, lf, scratch, coarse);
+    return;
+  }
   if (h->restriction == TPMG_RESTRICT_SUMMATION) {
     const Halo H = exchange(h, lf, u);
     tpmg::launch_resid_restrict_sum(h->ctx->launch(), h->vcoef(), F.coef(h->nz), h->xi, u, H, f,
@@ -363,6 +380,12 @@ void resid_restrict(tpmg_hierarchy h, int lf, const double* u, const double* f, 
 
 void restrict_plain(tpmg_hierarchy h, int lf, const double* fine, double* coarse) {
   Level& C = h->lv[lf - 1];
+  if (h->generic) {
+    tpmg::launch_restrict_gen(h->ctx->launch(), C.coef(h->nz), C.d_children.p, h->rule,
+                              h->lv[lf].plane, fine, coarse,
+                              h->restriction == TPMG_RESTRICT_TRANSPOSE);
+    return;
+  }
   if (h->restriction == TPMG_RESTRICT_SUMMATION) {
     tpmg::launch_restrict_sum(h->ctx->launch(), C.nx, C.ny, h->nz, fine, coarse);
   } else {
@@ -374,6 +397,12 @@ void restrict_plain(tpmg_hierarchy h, int lf, const double* fine, double* coarse
 void prolong_level(tpmg_hierarchy h, int lc, const double* coarse, double* fine, bool add) {
   Level& F = h->lv[lc + 1];
   const bool linear = h->prolongation == TPMG_PROLONG_LINEAR;
+  if (h->generic) {
+    Level& C = h->lv[lc];
+    tpmg::launch_prolong_gen(h->ctx->launch(), C.coef(h->nz), C.d_children.p, h->rule, F.plane,
+                             coarse, fine, linear, add);
+    return;
+  }
   const Halo Hc = linear ? exchange(h, lc, coarse) : Halo{};
   tpmg::launch_prolong(h->ctx->launch(), F.nx, F.ny, h->nz, coarse, Hc, fine, linear, add);
 }
@@ -983,6 +1012,99 @@ int tpmg_hier_create_full(tpmg_context ctx, const tpmg_grid_desc* g, const tpmg_
                           double omega, const tpmg_mg_config* cfg, tpmg_hierarchy* out) {
   if (!fp) return hier_create_impl(ctx, nullptr, nullptr, nullptr, nullptr, omega, cfg, out);
   return hier_create_impl(ctx, g, nullptr, fp, nullptr, omega, cfg, out);
+}
+
+int tpmg_hier_create_generic(tpmg_context ctx, int n_levels, int nz, int nnb, int nchild,
+                             const int64_t* ncells, const int64_t* nedges,
+                             const int64_t* const* nbr, const int64_t* const* cedge,
+                             const int64_t* const* children, const int* prol_d1,
+                             const int* prol_d2, const double* bv, const double* sv,
+                             const double* av, const double* xv, const double* const* bh,
+                             const double* const* ah, const double* const* xh,
+                             const double* const* sh, double relax, int prolongation,
+                             int restriction, int nu_pre, int nu_post, tpmg_hierarchy* out) {
+  return guard(ctx, [&] {
+    if (!ctx || !ncells || !nedges || !nbr || !cedge || !bv || !sv || !av || !xv || !bh || !ah ||
+        !xh || !sh || !out)
+      throw Error(TPMG_E_CONFIG, "null argument");
+    if (ctx->world != 1) throw Error(TPMG_E_CONFIG, "indirect hierarchies run on one rank");
+    if (n_levels < 1 || nz < 1 || nnb < 1 || nnb > 8 || nchild < 1 || nchild > 8)
+      throw Error(TPMG_E_CONFIG, "bad table sizes (1 <= nnb, nchild <= 8)");
+    if (!(relax > 0.0 && relax < 2.0))
+      throw Error(TPMG_E_CONFIG, "smoother relaxation factor must lie in (0, 2)");
+    if (n_levels > 1 && (!children || !prol_d1 || !prol_d2))
+      throw Error(TPMG_E_CONFIG, "child tables and the prolongation rule are required");
+    CUDA_CHECK(cudaSetDevice(ctx->device));
+    auto h = std::make_unique<tpmg_hierarchy_s>();
+    h->ctx = ctx;
+    h->nz = nz;
+    h->xi = true;  // the reference's build_column always carries the xi terms
+    h->generic = true;
+    h->relax = relax;
+    h->prolongation = prolongation;
+    h->restriction = restriction;
+    h->lv.resize(n_levels);
+    h->nu_pre.assign(n_levels, nu_pre);
+    h->nu_post.assign(n_levels, nu_post);
+    h->nu_pre[0] = 1;  // multigrid.hpp:269-270
+    h->nu_post[0] = 0;
+    h->rule.nchild = nchild;
+    for (int j = 0; j < nchild; ++j) {
+      h->rule.d1[j] = prol_d1 ? prol_d1[j] : -1;
+      h->rule.d2[j] = prol_d2 ? prol_d2[j] : -1;
+      if (n_levels > 1 && h->rule.d1[j] >= nnb) throw Error(TPMG_E_CONFIG, "prolongation rule out of range");
+    }
+    check_finite(bv, nz, "bv"); check_finite(sv, nz, "sv");
+    check_finite(av, nz + 1, "av"); check_finite(xv, nz + 1, "xv");
+    h->bv.assign(bv, bv + nz); h->sv.assign(sv, sv + nz);
+    h->av.assign(av, av + nz + 1); h->xv.assign(xv, xv + nz + 1);
+    auto to_int = [](const int64_t* a, int64_t n, int64_t bound, const char* what) {
+      std::vector<int> v(n);
+      for (int64_t i = 0; i < n; ++i) {
+        if (a[i] < 0 || a[i] >= bound) throw Error(TPMG_E_SHAPE, std::string(what) + ": index out of range");
+        v[i] = (int)a[i];
+      }
+      return v;
+    };
+    int64_t max_blocks = 1024;
+    for (int l = 0; l < n_levels; ++l) {
+      Level& L = h->lv[l];
+      const int64_t nc = ncells[l], ne = nedges[l];
+      if (nc < 1 || nc > (1 << 30) || ne < 1) throw Error(TPMG_E_SHAPE, "bad level size");
+      L.nx = (int)nc; L.ny = 1; L.gnx = (int)nc; L.gny = 1; L.plane = nc;
+      L.nnb = nnb;
+      check_finite(bh[l], nc, "bh"); check_finite(ah[l], nc, "ah");
+      check_finite(xh[l], nc, "xh"); check_finite(sh[l], ne, "sh");
+      L.d_bh.upload(bh[l], nc); L.d_ah.upload(ah[l], nc); L.d_xh.upload(xh[l], nc);
+      L.d_shg.upload(sh[l], ne);
+      const auto vn = to_int(nbr[l], nc * nnb, nc, "neighbour table");
+      const auto ve = to_int(cedge[l], nc * nnb, ne, "edge table");
+      L.d_nbr.upload(vn.data(), vn.size());
+      L.d_cedge.upload(ve.data(), ve.size());
+      if (l + 1 < n_levels) {
+        const auto vc = to_int(children[l + 1], nc * nchild, ncells[l + 1], "child table");
+        L.d_children.upload(vc.data(), vc.size());
+      }
+      const int64_t n = nc * nz;
+      if (l < n_levels - 1) {
+        L.t.alloc(n); L.u.alloc(n); L.f.alloc(n);
+      }
+      max_blocks = std::max<int64_t>(max_blocks, (n + 255) / 256 + 1);
+    }
+    h->d_bv.upload(h->bv.data(), nz);
+    h->d_sv.upload(h->sv.data(), nz);
+    h->d_av.upload(h->av.data(), nz + 1);
+    h->d_xv.upload(h->xv.data(), nz + 1);
+    const int64_t nf = h->lv[n_levels - 1].plane * nz;
+    h->r.alloc(nf); h->z.alloc(nf); h->p.alloc(nf); h->q.alloc(nf); h->tmp.alloc(nf);
+    h->partials.alloc(std::max<int64_t>(max_blocks, 148 * 8));
+    h->scal.alloc(8);
+    CUDA_CHECK(cudaMemset(h->scal.p, 0, 8 * sizeof(double)));
+    CUDA_CHECK(cudaMalloc(&h->d_err, sizeof(int)));
+    CUDA_CHECK(cudaMemset(h->d_err, 0, sizeof(int)));
+    CUDA_CHECK(cudaMallocHost(&h->h_scal, 8 * sizeof(double)));
+    *out = h.release();
+  });
 }
 
 int tpmg_hier_coef_mode(tpmg_hierarchy h, int* mode) {

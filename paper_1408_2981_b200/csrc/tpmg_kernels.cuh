@@ -45,6 +45,20 @@ struct LevelCoef {     // HattedComponent::horiz, per column of the local tile
   const double* sed = nullptr;
   const double* ssd = nullptr;
   const double* snd = nullptr;
+  // indirect (unstructured) levels: the reference's HorizontalGrid tables (geometry.hpp:41-71);
+  // nbr == nullptr on the Cartesian levels.  plane = number of cells, nx = plane, ny = 1.
+  int nnb = 0;
+  const int* nbr = nullptr;    // plane x nnb: neighbour j of cell T at nbr[T*nnb + j]
+  const int* cedge = nullptr;  // plane x nnb: edge shared with that neighbour
+  const double* shg = nullptr; // alpha_s hat horizontal factor per edge
+};
+
+// Coarse-to-fine relation of an indirect hierarchy: children of the coarse cells
+// (GridHierarchy::child_of) and the prolongation's corner rule (multigrid.hpp:88-95): child j
+// blends the coarse neighbours in directions d1[j], d2[j]; d1[j] < 0 marks the centre child.
+struct GenRule {
+  int nchild;
+  int d1[8], d2[8];
 };
 
 // Where the neighbour values across each tile face live.  For direction d
@@ -118,6 +132,15 @@ void launch_pcg_ap(const Launch& L, const VertCoef& V, const LevelCoef& C, bool 
 enum VecLinOp { VL_P = 0, VL_AXMY = 1, VL_X2 = 2, VL_AXPY = 3, VL_ADD = 4 };
 void launch_vec_lin(const Launch& L, int op, int64_t n, double* y, const double* a,
                     const double* b, double s1, double s2);
+// Indirect levels (GenRule / LevelCoef::nbr): summation or transpose restriction from the fine
+// level and linear / injection prolongation (+=) into it; Cc is the coarse level,
+// `children` its child table on the fine level.
+void launch_restrict_gen(const Launch& L, const LevelCoef& Cc, const int* children,
+                         const GenRule& rule, int64_t fplane, const double* fine, double* coarse,
+                         bool transpose);
+void launch_prolong_gen(const Launch& L, const LevelCoef& Cc, const int* children,
+                        const GenRule& rule, int64_t fplane, const double* coarse, double* fine,
+                        bool linear, bool add);
 void launch_pcg_xfinal(const Launch& L, int64_t n, const double* s, const double* p, double* x);
 
 // coarse = R_sum(fine) (restrict_field, multigrid.hpp:29-43).

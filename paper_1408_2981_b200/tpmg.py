@@ -263,6 +263,48 @@ class Hierarchy:
         self.n_levels = n.value
         self.finest = self.n_levels - 1
 
+    @classmethod
+    def from_tables(cls, ctx: Context, nz, nnb, nchild, ncells, nedges, nbr, cedge, children,
+                    prol_d1, prol_d2, bv, sv, av, xv, bh, ah, xh, sh, relax, prolongation,
+                    restriction, nu_pre, nu_post) -> "Hierarchy":
+        """An indirect (e.g. icosahedral) hierarchy from the reference's grid tables and hatted
+        coefficients (tpmg_hier_create_generic); lists are per level, coarsest first."""
+        self = cls.__new__(cls)
+        self.ctx, self.lib = ctx, ctx.lib
+        self._h = None
+        nl = len(ncells)
+        I64P = C.POINTER(C.c_int64)
+        keep = []
+
+        def i64(a):
+            a = np.ascontiguousarray(a, dtype=np.int64)
+            keep.append(a)
+            return a.ctypes.data_as(I64P)
+
+        def f64(a):
+            a = np.ascontiguousarray(a, dtype=np.float64)
+            keep.append(a)
+            return a.ctypes.data_as(C.POINTER(C.c_double))
+
+        D = C.POINTER(C.c_double)
+        h = C.c_void_p()
+        ctx._check(self.lib.tpmg_hier_create_generic(
+            ctx._h, nl, int(nz), int(nnb), int(nchild), i64(ncells), i64(nedges),
+            (I64P * nl)(*[i64(a) for a in nbr]), (I64P * nl)(*[i64(a) for a in cedge]),
+            (I64P * nl)(*[i64(a) if a is not None else None for a in children]),
+            (C.c_int * nchild)(*prol_d1), (C.c_int * nchild)(*prol_d2), f64(bv), f64(sv), f64(av),
+            f64(xv), (D * nl)(*[f64(a) for a in bh]), (D * nl)(*[f64(a) for a in ah]),
+            (D * nl)(*[f64(a) for a in xh]), (D * nl)(*[f64(a) for a in sh]), C.c_double(relax),
+            int(prolongation), int(restriction), int(nu_pre), int(nu_post), C.byref(h)))
+        self._h = h
+        ctx._live_children += 1
+        self.problem = None
+        n = C.c_int()
+        self.lib.tpmg_hier_n_levels(self._h, C.byref(n))
+        self.n_levels = n.value
+        self.finest = self.n_levels - 1
+        return self
+
     def level_shape(self, level: int):
         v = [C.c_int64() for _ in range(5)]
         self.ctx._check(self.lib.tpmg_hier_level_shape(self._h, level, *[C.byref(x) for x in v]))

@@ -1,0 +1,97 @@
+"""The DEVICE path pinned against the REFERENCE ITSELF on the reference's own problem.
+
+tests/golden/ref_icosa_pin.bin holds the outputs of the reference's unmodified headers
+(compiled by oracle/build_ref.py) on its icosahedral hierarchy: 3 levels of 20 / 80 / 320
+triangles, nz = 8, balanced-flow factorised coefficients with vertical advection, geometric
+grading, block-Jacobi relax 0.9, nu = 2+2.  tpmg_hier_create_generic takes the same neighbour /
+edge / child tables and hatted coefficients, and the sm_100a indirect-level kernels must
+reproduce apply_operator, two block-Jacobi sweeps, both restrictions, both prolongations and
+whole V-cycles for the three transfer pairs BIT FOR BIT (test_ref_pin.py does the same for the
+CPU oracle).  The cycle rate is a norm-based diagnostic: 1e-12.
+"""
+import numpy as np
+import pytest
+
+from test_ref_pin import load
+from paper_1408_2981_b200 import tpmg
+from paper_1408_2981_b200.tpmg import K_FASTEST
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def R():
+    return load()
+
+
+def make(ctx, R, prolongation=0, restriction=0):
+    nl = int(R["n_levels"][0])
+    nz = int(R["nr"][0])
+    ncells = [len(R["bh%d" % l]) for l in range(nl)]
+    nedges = [len(R["sh%d" % l]) for l in range(nl)]
+    children = [None] + [np.arange(4 * ncells[l - 1], dtype=np.int64) for l in range(1, nl)]
+    return tpmg.Hierarchy.from_tables(
+        ctx, nz, 3, 4, ncells, nedges, [R["nbr%d" % l] for l in range(nl)],
+        [R["cedge%d" % l] for l in range(nl)], children, [1, 2, 0, -1], [2, 0, 1, -1],
+        R["bv"], R["sv"], R["av"], R["xv"], [R["bh%d" % l] for l in range(nl)],
+        [R["ah%d" % l] for l in range(nl)], [R["xh%d" % l] for l in range(nl)],
+        [R["sh%d" % l] for l in range(nl)], float(R["relax"][0]), prolongation, restriction,
+        2, 2)
+
+
+def same(a, b, what):
+    bad = np.flatnonzero(a != b)
+    assert bad.size == 0, f"{what}: {bad.size}/{a.size} differ, first {bad[:5]}, max |d| " \
+                          f"{np.max(np.abs(a - b)):.3e}"
+
+
+def test_apply_bitwise(gpu_ctx, R):
+    h = make(gpu_ctx, R)
+    y = h.field()
+    tpmg.apply_operator(h, h.field().upload(R["u"], K_FASTEST), y)
+    same(y.download(K_FASTEST), R["apply"], "apply_operator")
+
+
+def test_block_jacobi_bitwise(gpu_ctx, R):
+    h = make(gpu_ctx, R)
+    u = h.field().upload(R["u"], K_FASTEST)
+    tpmg.smooth(h, u, h.field().upload(R["f"], K_FASTEST), 2)
+    same(u.download(K_FASTEST), R["smooth2"], "smooth x2")
+
+
+@pytest.mark.parametrize("lc", [0, 1])
+def test_transfers_bitwise(gpu_ctx, R, lc):
+    s = str(lc)
+    for pr, rs, key_r, key_p in ((0, 0, "restrict_sum", "prolong_lin"),
+                                 (0, 1, "restrict_T", None), (1, 0, None, "prolong_inj")):
+        h = make(gpu_ctx, R, pr, rs)
+        fine, coarse = h.field(lc + 1), h.field(lc)
+        if key_r:
+            fine.upload(R["tr_fine" + s], K_FASTEST)
+            tpmg.restrict_field(h, fine, coarse)
+            same(coarse.download(K_FASTEST), R[key_r + s], key_r)
+        if key_p:
+            coarse.upload(R["tr_coarse" + s], K_FASTEST)
+            tpmg.prolongate_field(h, coarse, fine)
+            same(fine.download(K_FASTEST), R[key_p + s], key_p)
+
+
+@pytest.mark.parametrize("c,pr", [(0, (0, 0)), (1, (0, 1)), (2, (1, 0))])
+def test_vcycle_bitwise(gpu_ctx, R, c, pr):
+    h = make(gpu_ctx, R, *pr)
+    f = h.field().upload(R["f"], K_FASTEST)
+    u = h.field().upload(R["u0"], K_FASTEST)
+    tpmg.v_cycle(h, f, u)
+    same(u.download(K_FASTEST), R["vcycle%d" % c], "v_cycle")
+    rate = tpmg.measure_cycle_rate(h, f, 4)
+    assert abs(rate - R["rate%d" % c][0]) <= 1e-12 * abs(R["rate%d" % c][0])
+
+
+def test_outer_solvers_on_the_reference_problem(gpu_ctx, R):
+    """BiCGStab (the reference problem has vertical advection: A is not symmetric) with the
+    V-cycle preconditioner converges on the icosahedral grid."""
+    h = make(gpu_ctx, R, 0, 1)
+    f = h.field().upload(R["f"], K_FASTEST)
+    x = h.field()
+    res = tpmg.bicgstab_solve(h, f, x, 1e-10, 100)
+    assert res.status == 0 and res.history[-1] <= 1e-10 * res.history[0]
