@@ -261,6 +261,51 @@ int tpmg_solver_counts(tpmg_hierarchy h, int64_t* n_precond, int64_t* n_matvec);
 int tpmg_pcg_host(tpmg_hierarchy h, const double* f_host, double* x_host, int layout, double tol,
                   int max_iter, double* res_hist, int* iters, int* solve_status);
 
+/* ---- profile files: save_profiles / load_profiles (profile_io.hpp:125-242) ------------------ */
+/* The reference's JSON profile format, byte for byte as its writer (nlohmann dump(1): keys
+ * sorted, shortest round-trip doubles, non-finite -> null): format_version 1, kind "factorized" |
+ * "full", grid header {fingerprint, level, n_r, type}, arrays column-major with k fastest, as
+ * decimal numbers or "base64-f64le".  Host-only, no context needed.
+ * Arrays travel PACKED, back to back in this order (nc cells, ne edges):
+ *   factorized: beta_r nz, alpha_s_r nz, alpha_r_r nz+1, xi_r_r nz+1,
+ *               beta_s nc, alpha_r_s nc, xi_r_s nc, alpha_s_s ne
+ *   full:       beta nz*nc, alpha_s nz*ne, alpha_r (nz+1)*nc, xi_r (nz+1)*nc
+ * (each dense array k fastest, i.e. entry c*rows + k).  Load errors follow load_profiles, checked
+ * in its order: unreadable file -> TPMG_E_CONFIG; wrong grid -> TPMG_E_FINGERPRINT; n_r, level,
+ * kind, array length or malformed JSON -> TPMG_E_SHAPE; non-finite, null or non-numeric entry ->
+ * TPMG_E_NONFINITE; output buffer too small -> TPMG_E_CAP. */
+typedef enum tpmg_profile_kind { TPMG_PROFILE_FACTORIZED = 0, TPMG_PROFILE_FULL = 2 } tpmg_profile_kind;
+
+/* The grid header a file is written for / validated against (detail::grid_header,
+ * profile_io.hpp:114-121).  nx, ny > 0 are written as extra header keys (Cartesian grids). */
+typedef struct tpmg_profile_grid {
+  const char* type;     /* "icosahedral", "cartesian", ... */
+  uint64_t fingerprint; /* grid_fingerprint, geometry.hpp:335-351 */
+  int64_t level;
+  int64_t n_r, n_cells, n_edges;
+  int64_t nx, ny;       /* 0 = not written */
+} tpmg_profile_grid;
+
+/* grid_fingerprint (geometry.hpp:335-351): FNV-1a 64 over the bytes of the cell centres,
+ * centers[3*c + i] (the reference's Matrix3X, column-major). */
+uint64_t tpmg_grid_fingerprint(const double* centers, int64_t n_cells);
+/* The Cartesian analogue: centres ((i+1/2) hx, (j+1/2) hy, 0) in cell order j*nx + i. */
+uint64_t tpmg_grid_fingerprint_cartesian(const tpmg_grid_desc* grid);
+int64_t tpmg_profile_packed_size(int kind, int64_t n_cells, int64_t n_edges, int64_t n_r);
+/* Any grid (e.g. the reference's icosahedral levels, with tpmg_hier_create_generic). */
+int tpmg_profile_save_grid(const char* path, const tpmg_profile_grid* grid, int kind,
+                           const double* packed, int base64);
+int tpmg_profile_load_grid(const char* path, const tpmg_profile_grid* grid, int* kind,
+                           double* packed, int64_t capacity);
+/* The Cartesian grid of tpmg_hier_create: type "cartesian", level 0, n_cells = nx*ny,
+ * n_edges = 2*nx*ny (east edges, then north edges), fingerprint as above. */
+int tpmg_profile_save(const char* path, const tpmg_grid_desc* grid, int kind, const double* packed,
+                      int base64);
+int tpmg_profile_load(const char* path, const tpmg_grid_desc* grid, int* kind, double* packed,
+                      int64_t capacity);
+/* Message of the last failed tpmg_profile_* call on this thread. */
+const char* tpmg_profile_last_error(void);
+
 /* ---- instrumentation ------------------------------------------------------------------------ */
 /* Number of kernels this library launched on the context since creation. */
 int tpmg_kernel_launch_count(tpmg_context ctx, int64_t* out);

@@ -74,6 +74,14 @@ SIGNATURES = {
     "tpmg_kernel_launch_count": (C.c_int, [_VP, C.POINTER(C.c_int64)]),
     "tpmg_set_use_graphs": (C.c_int, [_VP, C.c_int]),
     "tpmg_time_kernel": (C.c_int, [_VP, C.c_int, C.c_int, C.c_int, _D]),
+    "tpmg_profile_packed_size": (C.c_int64, [C.c_int, C.c_int64, C.c_int64, C.c_int64]),
+    "tpmg_grid_fingerprint": (C.c_uint64, [_D, C.c_int64]),
+    "tpmg_grid_fingerprint_cartesian": (C.c_uint64, [C.c_void_p]),
+    "tpmg_profile_save_grid": (C.c_int, [C.c_char_p, C.c_void_p, C.c_int, _D, C.c_int]),
+    "tpmg_profile_load_grid": (C.c_int, [C.c_char_p, C.c_void_p, C.POINTER(C.c_int), _D, C.c_int64]),
+    "tpmg_profile_save": (C.c_int, [C.c_char_p, C.c_void_p, C.c_int, _D, C.c_int]),
+    "tpmg_profile_load": (C.c_int, [C.c_char_p, C.c_void_p, C.POINTER(C.c_int), _D, C.c_int64]),
+    "tpmg_profile_last_error": (C.c_char_p, []),
 }
 
 
@@ -94,6 +102,12 @@ class FactorizedProfiles(C.Structure):
 
 class FullProfiles(C.Structure):  # tpmg_full_profiles
     _fields_ = [(n, _D) for n in ("beta", "alpha_s", "alpha_r", "xi_r")]
+
+
+class ProfileGrid(C.Structure):  # tpmg_profile_grid
+    _fields_ = [("type", C.c_char_p), ("fingerprint", C.c_uint64), ("level", C.c_int64),
+                ("n_r", C.c_int64), ("n_cells", C.c_int64), ("n_edges", C.c_int64),
+                ("nx", C.c_int64), ("ny", C.c_int64)]
 
 
 class MGConfig(C.Structure):

@@ -470,3 +470,131 @@ def pcg_solve_host(h: Hierarchy, f_host: np.ndarray, tol: float, max_iter: int =
     h.ctx._check(h.lib.tpmg_pcg_host(h._h, _p(f_host), _p(x), layout, C.c_double(tol), max_iter,
                                      _p(hist), C.byref(it), C.byref(st)))
     return x, SolveResult(it.value, st.value, hist[: it.value + 1].copy(), 0.0)
+
+
+# ---- profile files: save_profiles / load_profiles (profile_io.hpp:125-242) ----------------------
+
+PROFILE_FACTORIZED, PROFILE_FULL = 0, 2
+PROFILE_ORDER = {
+    PROFILE_FACTORIZED: ("beta_r", "alpha_s_r", "alpha_r_r", "xi_r_r", "beta_s", "alpha_r_s",
+                         "xi_r_s", "alpha_s_s"),
+    PROFILE_FULL: ("beta", "alpha_s", "alpha_r", "xi_r"),
+}
+
+
+def _profile_shapes(kind: int, nc: int, ne: int, nr: int):
+    """Array shapes in the reference's Matrix order: dense arrays (cols, rows), k fastest."""
+    if kind == PROFILE_FACTORIZED:
+        return ((nr,), (nr,), (nr + 1,), (nr + 1,), (nc,), (nc,), (nc,), (ne,))
+    return ((nc, nr), (ne, nr), (nc, nr + 1), (nc, nr + 1))
+
+
+def _profile_call(rc: int):
+    if rc != OK:
+        msg = _capi.load().tpmg_profile_last_error().decode()
+        raise _ERRORS.get(rc, TpmgError)(msg)
+
+
+def grid_fingerprint(centers: np.ndarray) -> int:
+    """grid_fingerprint (geometry.hpp:335-351) of centres given as (n_cells, 3)."""
+    c = np.ascontiguousarray(centers, dtype=np.float64)
+    return int(_capi.load().tpmg_grid_fingerprint(_p(c), c.shape[0]))
+
+
+def profile_grid(type: str, fingerprint: int, level: int, n_r: int, n_cells: int, n_edges: int,
+                 nx: int = 0, ny: int = 0) -> _capi.ProfileGrid:
+    return _capi.ProfileGrid(type.encode(), fingerprint, level, n_r, n_cells, n_edges, nx, ny)
+
+
+def _packed(kind: int, grid, arrays: dict) -> np.ndarray:
+    shapes = _profile_shapes(kind, grid.n_cells, grid.n_edges, grid.n_r)
+    parts = []
+    for name, shape in zip(PROFILE_ORDER[kind], shapes):
+        a = np.asarray(arrays[name], dtype=np.float64)
+        if a.shape != shape:
+            raise shape_error(f"profile array {name!r} has shape {a.shape}, expected {shape}")
+        parts.append(a.ravel())
+    return np.ascontiguousarray(np.concatenate(parts))
+
+
+def _unpack(kind: int, grid, buf: np.ndarray) -> dict:
+    out, off = {}, 0
+    for name, shape in zip(PROFILE_ORDER[kind], _profile_shapes(kind, grid.n_cells, grid.n_edges,
+                                                                grid.n_r)):
+        n = int(np.prod(shape))
+        out[name] = buf[off:off + n].reshape(shape).copy()
+        off += n
+    return out
+
+
+def save_profile_arrays(path: str, grid, kind: int, arrays: dict,
+                        encoding: str = "decimal") -> None:
+    """save_profiles on any grid header (tpmg_profile_save_grid)."""
+    if encoding not in ("decimal", "base64-f64le"):
+        raise config_error(f"unknown encoding {encoding!r}")
+    packed = _packed(kind, grid, arrays)
+    _profile_call(_capi.load().tpmg_profile_save_grid(path.encode(), C.byref(grid), kind,
+                                                      _p(packed),
+                                                      int(encoding == "base64-f64le")))
+
+
+def load_profile_arrays(path: str, grid):
+    """load_profiles on any grid header: returns (kind, {name: array})."""
+    L = _capi.load()
+    cap = max(L.tpmg_profile_packed_size(k, grid.n_cells, grid.n_edges, grid.n_r)
+              for k in PROFILE_ORDER)
+    buf = np.empty(cap, dtype=np.float64)
+    kind = C.c_int()
+    _profile_call(L.tpmg_profile_load_grid(path.encode(), C.byref(grid), C.byref(kind), _p(buf),
+                                           cap))
+    return kind.value, _unpack(kind.value, grid, buf)
+
+
+def cartesian_profile_grid(P) -> _capi.ProfileGrid:
+    z = np.ascontiguousarray(P.z_faces, dtype=np.float64)
+    gd = GridDesc(P.nx, P.ny, P.hx, P.hy, P.nz, _p(z))
+    fp = int(_capi.load().tpmg_grid_fingerprint_cartesian(C.byref(gd)))
+    nc = P.nx * P.ny
+    return profile_grid("cartesian", fp, 0, P.nz, nc, 2 * nc, P.nx, P.ny)
+
+
+def save_profiles(path: str, P, encoding: str = "decimal") -> None:
+    """save_profiles (profile_io.hpp:125-165) of P's profile set on P's Cartesian grid: its
+    factorised profiles, or its dense ProfileSet when P.coef == "full".  encoding "decimal" or
+    "base64-f64le".  A None advection profile is written as zeros (the reference always stores
+    xi_r)."""
+    nc, nz = P.nx * P.ny, P.nz
+    if P.coef == "full":
+        d = dict(P.dense)
+        if d.get("xi_r") is None:
+            d["xi_r"] = np.zeros((nc, nz + 1))
+        kind, arrays = PROFILE_FULL, d
+    elif P.coef == "factorized":
+        arrays = {n: getattr(P, n) for n in PROFILE_ORDER[PROFILE_FACTORIZED]}
+        if arrays["xi_r_r"] is None or arrays["xi_r_s"] is None:
+            arrays["xi_r_r"], arrays["xi_r_s"] = np.zeros(nz + 1), np.zeros(nc)
+        kind = PROFILE_FACTORIZED
+    else:
+        raise config_error("the profile format stores factorised or full profile sets")
+    save_profile_arrays(path, cartesian_profile_grid(P), kind, arrays, encoding)
+
+
+def load_profiles(path: str, P):
+    """load_profiles (profile_io.hpp:168-242): read a profile file written for P's grid and return
+    a copy of P with those profiles (coef "factorized" or "full").  Raises fingerprint_error for
+    another grid, shape_error for wrong sizes or a malformed file, nonfinite_error for NaN/Inf/null,
+    config_error for an unreadable file.  All-zero advection arrays come back as None (xi = 0)."""
+    import dataclasses
+    kind, arrays = load_profile_arrays(path, cartesian_profile_grid(P))
+    Q = dataclasses.replace(P)
+    if kind == PROFILE_FACTORIZED:
+        if not arrays["xi_r_r"].any() or not arrays["xi_r_s"].any():
+            arrays["xi_r_r"] = arrays["xi_r_s"] = None
+        for k, v in arrays.items():
+            setattr(Q, k, v)
+        Q.coef, Q.dense = "factorized", None
+    else:
+        if not arrays["xi_r"].any():
+            arrays["xi_r"] = None
+        Q.coef, Q.dense = "full", arrays
+    return Q
