@@ -1,3 +1,4 @@
+#include <cstdio>
 // tpmg_host.cpp -- C-ABI implementation (include/tpmg_b200.h): hierarchy setup, device
 // resident fields, the V-cycle / PCG drivers and the NCCL halo + all-reduce plumbing.
 //
@@ -341,14 +342,14 @@ void apply_level(tpmg_hierarchy h, int l, int mode, const double* u, const doubl
 // One line-Jacobi sweep.  With `fz` the sweep also does fused PCG work (see PcgFuse) and its
 // per-tile partials are reduced into scalar slot `slot`.
 void sweep(tpmg_hierarchy h, int l, const double* u_in, const double* f, double* out,
-           const tpmg::PcgFuse* fz = nullptr, int slot = -1) {
+           const tpmg::PcgFuse* fz = nullptr, int slot = -1, const tpmg::ProSrc* pro = nullptr) {
   Level& L = h->lv[l];
   // the haloed input: u, or p when the zero-guess sweep forms q = A p itself
   Halo H = u_in ? exchange(h, l, u_in)
                 : (fz && fz->p ? exchange(h, l, fz->p) : tpmg::self_halo(out, L.nx, L.ny, L.plane));
   int nb = 0;
   tpmg::launch_jacobi(h->ctx->launch(), h->vcoef(), L.coef(h->nz), h->xi, u_in, H, f, out,
-                      h->relax, h->d_err, fz, &nb);
+                      h->relax, h->d_err, fz, &nb, pro);
   if (fz) finish_dot(h, nb, slot);
 }
 
@@ -450,16 +451,27 @@ void vcycle(tpmg_hierarchy h, int l, const double* f, double* A, double* B, bool
     sweep(h, l, cur, f, out);
     cur = out;
   }
+  // the prolongation rides in the first post-sweep where that kernel can take it (one rank)
+  tpmg::ProSrc pro;
+  bool fuse_pro = false;
   if (l > 0) {
     Level& C = h->lv[l - 1];
     resid_restrict(h, l, cur, f, C.f.p, other(cur));
     vcycle(h, l - 1, C.f.p, C.u.p, C.t.p, true);
-    prolong_level(h, l - 1, C.u.p, cur, true);
+    fuse_pro = npost > 0 && h->ctx->world == 1 && !h->generic &&
+               h->prolongation == TPMG_PROLONG_LINEAR && tpmg::jacobi_prolong_fusable(L.coef(h->nz));
+    if (fuse_pro) {
+      pro.ec = C.u.p;
+      pro.cnx = (int)C.nx;
+      pro.cny = (int)C.ny;
+    } else {
+      prolong_level(h, l - 1, C.u.p, cur, true);
+    }
   }
   for (int s = 0; s < npost; ++s) {
     double* out = other(cur);
     const bool last = pcg_fuse && s + 1 == npost;
-    sweep(h, l, cur, f, out, last ? &fz : nullptr, 3);
+    sweep(h, l, cur, f, out, last ? &fz : nullptr, 3, s == 0 && fuse_pro ? &pro : nullptr);
     cur = out;
   }
   if (cur != A)

@@ -109,13 +109,27 @@ struct PcgFuse {
   const double* p = nullptr;
 };
 
+// The V-cycle's prolongation fused into the first post-sweep (multigrid.hpp:294-295 then
+// :296-297): the sweep's input is u + P ec with k_prolong_flat's linear values and addition
+// order, formed on chip (u itself is not modified).  One rank (periodic wrap), linear
+// prolongation, Cartesian levels; ec is the next coarser level's correction (cnx x cny x nz).
+struct ProSrc {
+  const double* ec = nullptr;
+  int cnx = 0, cny = 0;
+};
+
 // One block-Jacobi line sweep (smooth, relaxation.hpp:77-97): out = u + relax * T^{-1}(f - A u);
-// u == nullptr means a zero initial guess.  Zero pivots set bit 1 in *err.
+// u == nullptr means a zero initial guess.  Zero pivots set bit 1 in *err.  pro: see ProSrc
+// (only where jacobi_prolong_fusable holds).
 void launch_jacobi(const Launch& L, const VertCoef& V, const LevelCoef& C, bool xi,
                    const double* u, const Halo& H, const double* f, double* out, double relax,
-                   int* err, const PcgFuse* fuse = nullptr, int* nblocks = nullptr);
+                   int* err, const PcgFuse* fuse = nullptr, int* nblocks = nullptr,
+                   const ProSrc* pro = nullptr);
 // True when launch_jacobi takes the tiled TMEM path on this level (the fused PCG modes).
 bool jacobi_fusable(const LevelCoef& C);
+// True when a post-sweep on this level can take the prolongation (TMA tiled path, factorised
+// coefficients; TPMG_FUSE_PRO=0 disables).
+bool jacobi_prolong_fusable(const LevelCoef& C);
 
 // x += alpha p_old; p = z + beta p_old   (alpha = s[0]/s[1], beta = s[3]/s[0])
 void launch_pcg_px(const Launch& L, int64_t n, const double* s, const double* z, double* p,
