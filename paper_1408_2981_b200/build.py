@@ -18,10 +18,10 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 SOURCES = [os.path.join(CSRC, "tpmg_kernels.cu"), os.path.join(CSRC, "tpmg_host.cpp"),
-           os.path.join(CSRC, "tpmg_io.cpp")]
+           os.path.join(CSRC, "tpmg_io.cpp"), os.path.join(CSRC, "tpmg_icosa.cpp")]
 DEPS = SOURCES + [os.path.join(CSRC, "tpmg_kernels.cuh"), os.path.join(ROOT, "include", "tpmg_b200.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-shared",
+COMMON = ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC,-O3,-ffp-contract=off", "-shared",
           f"-I{os.path.join(ROOT, 'include')}", "-ldl"]
 
 

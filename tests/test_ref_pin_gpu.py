@@ -24,7 +24,23 @@ def R():
     return load()
 
 
-def make(ctx, R, prolongation=0, restriction=0):
+# The hierarchy either from the reference's dumped tables and coefficients ("tables") or from
+# the library's own host setup of the same problem ("setup": tpmg_icosa_create with the
+# reference driver's parameters, oracle/ref_driver.cpp) -- both must reproduce the reference.
+@pytest.fixture(params=["tables", "setup"])
+def source(request):
+    return request.param
+
+
+_ICO = {}
+
+
+def make(ctx, R, prolongation=0, restriction=0, source="tables"):
+    if source == "setup":
+        if "ico" not in _ICO:
+            _ICO["ico"] = tpmg.Icosahedral(2, int(R["nr"][0]), 80.0 / 6371.229, "geometric", 1.2,
+                                           0.022, 10.0, True)
+        return _ICO["ico"].hierarchy(ctx, 0, float(R["relax"][0]), prolongation, restriction, 2, 2)
     nl = int(R["n_levels"][0])
     nz = int(R["nr"][0])
     ncells = [len(R["bh%d" % l]) for l in range(nl)]
@@ -45,26 +61,26 @@ def same(a, b, what):
                           f"{np.max(np.abs(a - b)):.3e}"
 
 
-def test_apply_bitwise(gpu_ctx, R):
-    h = make(gpu_ctx, R)
+def test_apply_bitwise(gpu_ctx, R, source):
+    h = make(gpu_ctx, R, source=source)
     y = h.field()
     tpmg.apply_operator(h, h.field().upload(R["u"], K_FASTEST), y)
     same(y.download(K_FASTEST), R["apply"], "apply_operator")
 
 
-def test_block_jacobi_bitwise(gpu_ctx, R):
-    h = make(gpu_ctx, R)
+def test_block_jacobi_bitwise(gpu_ctx, R, source):
+    h = make(gpu_ctx, R, source=source)
     u = h.field().upload(R["u"], K_FASTEST)
     tpmg.smooth(h, u, h.field().upload(R["f"], K_FASTEST), 2)
     same(u.download(K_FASTEST), R["smooth2"], "smooth x2")
 
 
 @pytest.mark.parametrize("lc", [0, 1])
-def test_transfers_bitwise(gpu_ctx, R, lc):
+def test_transfers_bitwise(gpu_ctx, R, lc, source):
     s = str(lc)
     for pr, rs, key_r, key_p in ((0, 0, "restrict_sum", "prolong_lin"),
                                  (0, 1, "restrict_T", None), (1, 0, None, "prolong_inj")):
-        h = make(gpu_ctx, R, pr, rs)
+        h = make(gpu_ctx, R, pr, rs, source)
         fine, coarse = h.field(lc + 1), h.field(lc)
         if key_r:
             fine.upload(R["tr_fine" + s], K_FASTEST)
@@ -77,8 +93,8 @@ def test_transfers_bitwise(gpu_ctx, R, lc):
 
 
 @pytest.mark.parametrize("c,pr", [(0, (0, 0)), (1, (0, 1)), (2, (1, 0))])
-def test_vcycle_bitwise(gpu_ctx, R, c, pr):
-    h = make(gpu_ctx, R, *pr)
+def test_vcycle_bitwise(gpu_ctx, R, c, pr, source):
+    h = make(gpu_ctx, R, *pr, source=source)
     f = h.field().upload(R["f"], K_FASTEST)
     u = h.field().upload(R["u0"], K_FASTEST)
     tpmg.v_cycle(h, f, u)
@@ -87,10 +103,10 @@ def test_vcycle_bitwise(gpu_ctx, R, c, pr):
     assert abs(rate - R["rate%d" % c][0]) <= 1e-12 * abs(R["rate%d" % c][0])
 
 
-def test_outer_solvers_on_the_reference_problem(gpu_ctx, R):
+def test_outer_solvers_on_the_reference_problem(gpu_ctx, R, source):
     """BiCGStab (the reference problem has vertical advection: A is not symmetric) with the
     V-cycle preconditioner converges on the icosahedral grid."""
-    h = make(gpu_ctx, R, 0, 1)
+    h = make(gpu_ctx, R, 0, 1, source)
     f = h.field().upload(R["f"], K_FASTEST)
     x = h.field()
     res = tpmg.bicgstab_solve(h, f, x, 1e-10, 100)
