@@ -137,6 +137,9 @@ _libs: dict = {}
 
 
 def lib_path(variant: str = "exact") -> str:
+    # TPMG_LIB_PATH: an alternative build of the product library (A/B kernel timing only)
+    if variant == "exact" and os.environ.get("TPMG_LIB_PATH"):
+        return os.environ["TPMG_LIB_PATH"]
     return os.path.join(PKG_DIR, LIB_NAMES[variant])
 
 
