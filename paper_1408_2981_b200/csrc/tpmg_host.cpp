@@ -641,6 +641,7 @@ int tpmg_init(const tpmg_context_params* prm, tpmg_context* out) {
     ctx->rx = prm->rank % prm->px;
     ctx->ry = prm->rank / prm->px;
     CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    tpmg::init_device_constants(ctx->stream);
     if (ctx->world > 1) {
       if (!prm->nccl_id) throw Error(TPMG_E_CONFIG, "world_size > 1 needs an ncclUniqueId");
       g_nccl.load();

@@ -121,6 +121,9 @@ struct ProSrc {
 // One block-Jacobi line sweep (smooth, relaxation.hpp:77-97): out = u + relax * T^{-1}(f - A u);
 // u == nullptr means a zero initial guess.  Zero pivots set bit 1 in *err.  pro: see ProSrc
 // (only where jacobi_prolong_fusable holds).
+// one-time device constants (L2 cache policies); called at context creation, outside any
+// graph capture
+void init_device_constants(cudaStream_t st);
 void launch_jacobi(const Launch& L, const VertCoef& V, const LevelCoef& C, bool xi,
                    const double* u, const Halo& H, const double* f, double* out, double relax,
                    int* err, const PcgFuse* fuse = nullptr, int* nblocks = nullptr,
