@@ -172,7 +172,7 @@ struct tpmg_hierarchy_s {
   std::vector<int> nu_pre, nu_post;
   std::vector<Level> lv;  // coarsest .. finest
   std::vector<double> bv, sv, av, xv;
-  DevBuf d_bv, d_sv, d_av, d_xv;
+  DevBuf d_bv, d_sv, d_av, d_xv, d_vr, d_vx;
   // finest-level PCG / V-cycle work vectors
   DevBuf r, z, p, q, tmp;
   DevBuf p2;                // second search-direction buffer of the fused A p pass (ping-pong)
@@ -194,7 +194,27 @@ struct tpmg_hierarchy_s {
   std::unordered_map<const void*, cudaGraphExec_t> iter_graphs;
   std::unordered_map<const void*, int64_t> iter_graph_kernels;
   int finest() const { return (int)lv.size() - 1; }
-  VertCoef vcoef() const { return VertCoef{d_bv.p, d_sv.p, d_av.p, d_xv.p}; }
+  VertCoef vcoef() const {
+    VertCoef v{d_bv.p, d_sv.p, d_av.p, d_xv.p};
+    v.vr = d_vr.p;
+    v.vx = d_vx.p;
+    return v;
+  }
+  // interleaved copies of the vertical vectors (VertCoef::vr / vx) for the kernels' bulk staging
+  void upload_vertical_rows() {
+    const size_t nzz = bv.size();
+    std::vector<double> vr(4 * nzz), vx(2 * nzz);
+    for (size_t k = 0; k < nzz; ++k) {
+      vr[4 * k] = bv[k];
+      vr[4 * k + 1] = sv[k];
+      vr[4 * k + 2] = av[k];
+      vr[4 * k + 3] = av[k + 1];
+      vx[2 * k] = xv[k];
+      vx[2 * k + 1] = xv[k + 1];
+    }
+    d_vr.upload(vr.data(), vr.size());
+    d_vx.upload(vx.data(), vx.size());
+  }
   ~tpmg_hierarchy_s() {
     for (auto& kv : iter_graphs) cudaGraphExecDestroy(kv.second);
     if (d_err) cudaFree(d_err);
@@ -955,6 +975,7 @@ int hier_create_impl(tpmg_context ctx, const tpmg_grid_desc* g, const tpmg_facto
     h->d_sv.upload(h->sv.data(), nz);
     h->d_av.upload(h->av.data(), nz + 1);
     h->d_xv.upload(h->xv.data(), nz + 1);
+    h->upload_vertical_rows();
 
     // work buffers
     int64_t max_blocks = 1024;
@@ -1108,6 +1129,7 @@ int tpmg_hier_create_generic(tpmg_context ctx, int n_levels, int nz, int nnb, in
     h->d_sv.upload(h->sv.data(), nz);
     h->d_av.upload(h->av.data(), nz + 1);
     h->d_xv.upload(h->xv.data(), nz + 1);
+    h->upload_vertical_rows();
     const int64_t nf = h->lv[n_levels - 1].plane * nz;
     h->r.alloc(nf); h->z.alloc(nf); h->p.alloc(nf); h->q.alloc(nf); h->tmp.alloc(nf);
     h->partials.alloc(std::max<int64_t>(max_blocks, 148 * 8));

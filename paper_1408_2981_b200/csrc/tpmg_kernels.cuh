@@ -19,6 +19,10 @@ struct VertCoef {      // HattedComponent::vert of beta, alpha_s, alpha_r, xi_r
   const double* sv;    // nz
   const double* av;    // nz+1
   const double* xv;    // nz+1 (only read when the level has advection)
+  // the same, interleaved for one bulk copy into shared memory: vr[k] = {bv_k, sv_k, av_k,
+  // av_k+1}, vx[k] = {xv_k, xv_k+1} (nullptr: the kernels stage from the arrays above)
+  const double* vr = nullptr;
+  const double* vx = nullptr;
 };
 
 // Coefficient storage of a level (HattedComponent, discretization.hpp:32-48): factorised
