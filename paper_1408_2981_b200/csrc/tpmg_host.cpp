@@ -121,6 +121,11 @@ struct DevBufT {
     alloc(count);
     CUDA_CHECK(cudaMemcpy(p, h, count * sizeof(T), cudaMemcpyHostToDevice));
   }
+  void reset() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
   ~DevBufT() {
     if (p) cudaFree(p);
   }
@@ -145,6 +150,7 @@ struct Level {
   DevBuf d_shg;
   DevBuf u, t, f;              // V-cycle work: home iterate, ping-pong partner, rhs
   DevBuf send, recv;           // multi-GPU face buffers [W|E|S|N]
+  DevBuf d_piv, d_cpt;         // coarse levels: pre-factorised column blocks (LevelCoef::piv)
   LevelCoef coef(int nz) const {
     LevelCoef c;
     c.nx = nx; c.ny = ny; c.nz = nz; c.plane = plane;
@@ -154,6 +160,7 @@ struct Level {
     c.ard = d_ard.p; c.bd = d_bd.p; c.xid = d_xid.p;
     c.swd = d_swd.p; c.sed = d_sed.p; c.ssd = d_ssd.p; c.snd = d_snd.p;
     c.nnb = nnb; c.nbr = d_nbr.p; c.cedge = d_cedge.p; c.shg = d_shg.p;
+    c.piv = d_piv.p; c.cpt = d_cpt.p;
     return c;
   }
 };
@@ -1004,6 +1011,34 @@ int hier_create_impl(tpmg_context ctx, const tpmg_grid_desc* g, const tpmg_facto
     CUDA_CHECK(cudaMalloc(&h->d_err, sizeof(int)));
     CUDA_CHECK(cudaMemset(h->d_err, 0, sizeof(int)));
     CUDA_CHECK(cudaMallocHost(&h->h_scal, 8 * sizeof(double)));
+    // Coarse levels (the warp-per-column regime, L2 resident): the column blocks' Thomas
+    // factorisation is formed once here, so their sweeps only carry the right-hand side through
+    // the recurrence (TPMG_PIV=0 disables); a level with a zero pivot keeps the on-the-fly
+    // smoother (which raises the reference's singular_error when it is used)
+    {
+      const char* e = getenv("TPMG_PIV");
+      const bool use = !(e && atoi(e) == 0);
+      for (int l = 0; l < levels && use; ++l) {
+        Level& L = h->lv[l];
+        if (l == levels - 1 || !tpmg::jacobi_wants_factors(L.coef(nz))) continue;
+        L.d_piv.alloc(L.plane * nz);
+        L.d_cpt.alloc(L.plane * nz);
+        CUDA_CHECK(cudaMemsetAsync(h->d_err, 0, sizeof(int), ctx->stream));
+        LevelCoef c = L.coef(nz);
+        c.piv = c.cpt = nullptr;
+        tpmg::launch_factor_columns(ctx->launch(), h->vcoef(), c, h->xi, L.d_piv.p, L.d_cpt.p,
+                                    h->d_err);
+        int zero = 0;
+        CUDA_CHECK(cudaMemcpyAsync(&zero, h->d_err, sizeof(int), cudaMemcpyDeviceToHost,
+                                   ctx->stream));
+        CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        if (zero) {
+          L.d_piv.reset();
+          L.d_cpt.reset();
+        }
+      }
+      CUDA_CHECK(cudaMemset(h->d_err, 0, sizeof(int)));
+    }
     {
       const int L = levels - 1;
       const char* e = getenv("TPMG_PCG_FUSED");

@@ -55,6 +55,11 @@ struct LevelCoef {     // HattedComponent::horiz, per column of the local tile
   const int* nbr = nullptr;    // plane x nnb: neighbour j of cell T at nbr[T*nnb + j]
   const int* cedge = nullptr;  // plane x nnb: edge shared with that neighbour
   const double* shg = nullptr; // alpha_s hat horizontal factor per edge
+  // coarse levels: the column blocks' Thomas factorisation, fixed for the hierarchy's life
+  // (pivot_k and c'_k of thomas_solve_inplace, relaxation.hpp:42-48, [k][y][x]); nullptr: the
+  // smoother forms it on the fly
+  const double* piv = nullptr;
+  const double* cpt = nullptr;
 };
 
 // Coarse-to-fine relation of an indirect hierarchy: children of the coarse cells
@@ -125,6 +130,13 @@ struct ProSrc {
 // One block-Jacobi line sweep (smooth, relaxation.hpp:77-97): out = u + relax * T^{-1}(f - A u);
 // u == nullptr means a zero initial guess.  Zero pivots set bit 1 in *err.  pro: see ProSrc
 // (only where jacobi_prolong_fusable holds).
+// Thomas factorisation of every column block of a Cartesian level into piv / cpt (C.piv, C.cpt
+// must point to nz*plane doubles each); *zero_pivot set when a pivot vanishes (the caller then
+// keeps the on-the-fly smoother, which raises the singular error)
+void launch_factor_columns(const Launch& L, const VertCoef& V, const LevelCoef& C, bool xi,
+                           double* piv, double* cpt, int* zero_pivot);
+// levels whose sweeps take the pre-factorised warp-per-column path when factors exist
+bool jacobi_wants_factors(const LevelCoef& C);
 // one-time device constants (L2 cache policies); called at context creation, outside any
 // graph capture
 void init_device_constants(cudaStream_t st);
