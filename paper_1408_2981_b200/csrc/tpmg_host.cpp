@@ -200,6 +200,14 @@ struct tpmg_hierarchy_s {
   // one graph per (iterate buffer, direction parity): key = (const char*)x + pcur
   std::unordered_map<const void*, cudaGraphExec_t> iter_graphs;
   std::unordered_map<const void*, int64_t> iter_graph_kernels;
+  // device-side PCG loop (iterations 2..): one graph per iterate buffer, a while-node whose body
+  // holds two iterations (both direction parities), the second behind an if-node
+  std::unordered_map<const void*, cudaGraphExec_t> loop_graphs;
+  int64_t loop_kernels_per_iter = 0;
+  tpmg::PcgLoop* d_loop = nullptr;
+  tpmg::PcgLoop* h_loop = nullptr;  // pinned
+  DevBuf d_hist;                    // |r| per iteration, kLoopHist entries
+  static constexpr int kLoopHist = 4096;
   int finest() const { return (int)lv.size() - 1; }
   VertCoef vcoef() const {
     VertCoef v{d_bv.p, d_sv.p, d_av.p, d_xv.p};
@@ -224,6 +232,9 @@ struct tpmg_hierarchy_s {
   }
   ~tpmg_hierarchy_s() {
     for (auto& kv : iter_graphs) cudaGraphExecDestroy(kv.second);
+    for (auto& kv : loop_graphs) cudaGraphExecDestroy(kv.second);
+    if (d_loop) cudaFree(d_loop);
+    if (h_loop) cudaFreeHost(h_loop);
     if (d_err) cudaFree(d_err);
     if (h_scal) cudaFreeHost(h_scal);
   }
@@ -507,9 +518,12 @@ void vcycle(tpmg_hierarchy h, int l, const double* f, double* A, double* B, bool
 }
 
 void sync_check(tpmg_hierarchy h) {
+  // the error flag rides behind the queued work into pinned memory: one synchronisation
+  int* h_err = reinterpret_cast<int*>(h->h_scal + 7);
+  CUDA_CHECK(cudaMemcpyAsync(h_err, h->d_err, sizeof(int), cudaMemcpyDeviceToHost,
+                             h->ctx->stream));
   CUDA_CHECK(cudaStreamSynchronize(h->ctx->stream));
-  int err = 0;
-  CUDA_CHECK(cudaMemcpy(&err, h->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+  const int err = *h_err;
   if (err) {
     CUDA_CHECK(cudaMemset(h->d_err, 0, sizeof(int)));
     throw Error(TPMG_E_SINGULAR, "thomas_solve: zero pivot");
@@ -611,6 +625,88 @@ void run_iteration(tpmg_hierarchy h, double* x, bool first) {
   }
   CUDA_CHECK(cudaGraphLaunch(it->second, ctx->stream));
   ctx->launches += h->iter_graph_kernels[key];
+}
+
+// Opt-in (TPMG_DEVLOOP=1, read per solve): measured no faster than the host loop once its
+// per-iteration synchronisation was reduced to one, and ncu does not profile kernels inside
+// conditional graph bodies, so the evidence pipeline keeps the host loop by default.
+bool device_loop_ok(tpmg_hierarchy h, int max_iter) {
+  const char* e = getenv("TPMG_DEVLOOP");
+  const int env = e ? atoi(e) : 0;
+  return env != 0 && h->use_graphs && h->pcg_fused && h->ctx->world == 1 &&
+         max_iter < tpmg_hierarchy_s::kLoopHist;
+}
+
+cudaGraphExec_t loop_graph(tpmg_hierarchy h, double* x) {
+  auto found = h->loop_graphs.find(x);
+  if (found != h->loop_graphs.end()) return found->second;
+  tpmg_context ctx = h->ctx;
+  cudaStream_t s = ctx->stream;
+  if (!h->d_loop) {
+    CUDA_CHECK(cudaMalloc(&h->d_loop, sizeof(tpmg::PcgLoop)));
+    CUDA_CHECK(cudaMallocHost(&h->h_loop, sizeof(tpmg::PcgLoop)));
+    h->d_hist.alloc(tpmg_hierarchy_s::kLoopHist);
+  }
+  cudaGraph_t g;
+  CUDA_CHECK(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle hw, hi;
+  CUDA_CHECK(cudaGraphConditionalHandleCreate(&hw, g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams wp{};
+  wp.type = cudaGraphNodeTypeConditional;
+  wp.conditional.handle = hw;
+  wp.conditional.type = cudaGraphCondTypeWhile;
+  wp.conditional.size = 1;
+  cudaGraphNode_t wn;
+  CUDA_CHECK(cudaGraphAddNode(&wn, g, nullptr, 0, &wp));
+  cudaGraph_t body = wp.conditional.phGraph_out[0];
+  CUDA_CHECK(cudaGraphConditionalHandleCreate(&hi, body, 0, 0));
+  const int64_t before = ctx->launches;
+  // first half: direction parity 0, then the test (which also arms the second half)
+  CUDA_CHECK(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeThreadLocal));
+  std::vector<cudaGraphNode_t> tail;
+  try {
+    pcg_iteration(h, x, false, 0);
+    tpmg::launch_pcg_check(ctx->launch(), h->scal.p, h->d_hist.p, h->d_loop, hw, hi, 1);
+    cudaStreamCaptureStatus cs;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    CUDA_CHECK(cudaStreamGetCaptureInfo(s, &cs, nullptr, nullptr, &deps, &nd));
+    tail.assign(deps, deps + nd);
+  } catch (...) {
+    cudaStreamEndCapture(s, &body);
+    cudaGraphDestroy(g);
+    throw;
+  }
+  CUDA_CHECK(cudaStreamEndCapture(s, &body));
+  const int64_t per_iter = ctx->launches - before;
+  cudaGraphNodeParams ip{};
+  ip.type = cudaGraphNodeTypeConditional;
+  ip.conditional.handle = hi;
+  ip.conditional.type = cudaGraphCondTypeIf;
+  ip.conditional.size = 1;
+  cudaGraphNode_t in;
+  CUDA_CHECK(cudaGraphAddNode(&in, body, tail.data(), tail.size(), &ip));
+  cudaGraph_t ibody = ip.conditional.phGraph_out[0];
+  // second half: the other parity (the fused A p pass alternates the direction buffers)
+  CUDA_CHECK(cudaStreamBeginCaptureToGraph(s, ibody, nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeThreadLocal));
+  try {
+    pcg_iteration(h, x, false, h->fused_ap ? 1 : 0);
+    tpmg::launch_pcg_check(ctx->launch(), h->scal.p, h->d_hist.p, h->d_loop, hw, hi, 0);
+  } catch (...) {
+    cudaStreamEndCapture(s, &ibody);
+    cudaGraphDestroy(g);
+    throw;
+  }
+  CUDA_CHECK(cudaStreamEndCapture(s, &ibody));
+  ctx->launches = before;
+  h->loop_kernels_per_iter = per_iter;
+  cudaGraphExec_t ge;
+  CUDA_CHECK(cudaGraphInstantiate(&ge, g, 0));
+  cudaGraphDestroy(g);
+  h->loop_graphs.emplace(x, ge);
+  return ge;
 }
 
 }  // namespace
@@ -1466,6 +1562,32 @@ int tpmg_pcg(tpmg_hierarchy h, tpmg_field f, tpmg_field x, double tol, int max_i
       }
     };
     for (int it = 1; it <= max_iter; ++it) {
+      if (it == 2 && device_loop_ok(h, max_iter)) {
+        // iterations 2.. as one graph launch: the convergence test runs on the device
+        cudaGraphExec_t ge = loop_graph(h, x->buf.p);
+        *h->h_loop = tpmg::PcgLoop{r0, tol, max_iter, 1, 1, 0};
+        CUDA_CHECK(cudaMemcpyAsync(h->d_loop, h->h_loop, sizeof(tpmg::PcgLoop),
+                                   cudaMemcpyHostToDevice, s));
+        CUDA_CHECK(cudaGraphLaunch(ge, s));
+        CUDA_CHECK(cudaMemcpyAsync(h->h_loop, h->d_loop, sizeof(tpmg::PcgLoop),
+                                   cudaMemcpyDeviceToHost, s));
+        sync_check(h);
+        const tpmg::PcgLoop st = *h->h_loop;
+        const int ran = st.it - 1;  // iterations executed by the graph
+        ctx->launches += (int64_t)ran * h->loop_kernels_per_iter;
+        if (h->fused_ap && (ran & 1)) h->pcur ^= 1;
+        if (res_hist && st.iters >= 2)
+          CUDA_CHECK(cudaMemcpy(res_hist + 2, h->d_hist.p + 2, (st.iters - 1) * sizeof(double),
+                                cudaMemcpyDeviceToHost));
+        *iters = st.iters;
+        switch (st.exit) {
+          case 1: finish_x(); return;
+          case 2: *solve_status = TPMG_DIVERGED; finish_x(); return;
+          case 3: *solve_status = TPMG_BREAKDOWN; finish_x(); return;
+          case 4: *solve_status = TPMG_BREAKDOWN; return;
+          default: *solve_status = TPMG_NOT_CONVERGED; finish_x(); return;
+        }
+      }
       run_iteration(h, x->buf.p, it == 1);
       CUDA_CHECK(cudaMemcpyAsync(h->h_scal, h->scal.p, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
       sync_check(h);

@@ -135,6 +135,15 @@ struct ProSrc {
 // keeps the on-the-fly smoother, which raises the singular error)
 void launch_factor_columns(const Launch& L, const VertCoef& V, const LevelCoef& C, bool xi,
                            double* piv, double* cpt, int* zero_pivot);
+// Device-side PCG loop state (tpmg_pcg's convergence logic run by k_pcg_check inside a CUDA
+// graph while-node: no host round trip per iteration).  exit: 0 continue, 1 converged,
+// 2 diverged, 3 breakdown (rho), 4 breakdown (p.q, x not finalised), 5 iteration cap.
+struct PcgLoop {
+  double r0, tol;
+  int max_iter, it, iters, exit;
+};
+void launch_pcg_check(const Launch& L, const double* scal, double* hist, PcgLoop* st,
+                      unsigned long long hw, unsigned long long hi, int use_hi);
 // levels whose sweeps take the pre-factorised warp-per-column path when factors exist
 bool jacobi_wants_factors(const LevelCoef& C);
 // one-time device constants (L2 cache policies); called at context creation, outside any
