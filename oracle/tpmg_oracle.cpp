@@ -145,6 +145,32 @@ void thomas(Index n, const double* diag, const double* upper, const double* lowe
   for (Index k = n - 2; k >= 0; --k) x[k] -= scratch[k + 1] * x[k + 1];
 }
 
+// thomas() plus the r.z column sum of the fused finest post-sweep (k_jacobi_t3 PCGF 2):
+// r.z = sum_k r_k u_k + relax sum_k w_k d'_k, with d' the forward pass's values and
+// w_k = r_k - c'_k w_{k-1} (w = U^-T r, U the unit upper factor; c'_0 = 0, w_{-1} = 0), both
+// sums ascending in k; equal to sum_k r_k (u_k + relax x_k) in exact arithmetic.
+void thomas_rz(Index n, const double* diag, const double* upper, const double* lower, double* x,
+               double* scratch, const double* r, const double* u, double relax, double* colsum) {
+  double pivot = diag[0];
+  if (pivot == 0.0) throw Error(E_SINGULAR, "thomas_solve: zero pivot at row 0");
+  x[0] /= pivot;
+  for (Index k = 1; k < n; ++k) {
+    scratch[k] = upper[k - 1] / pivot;
+    pivot = diag[k] - lower[k] * scratch[k];
+    if (pivot == 0.0)
+      throw Error(E_SINGULAR, "thomas_solve: zero pivot at row " + std::to_string(k));
+    x[k] = (x[k] - lower[k] * x[k - 1]) / pivot;
+  }
+  double su = 0.0, sw = 0.0, w = 0.0;
+  for (Index k = 0; k < n; ++k) {
+    su += r[k] * u[k];
+    w = r[k] - (k == 0 ? 0.0 : scratch[k]) * w;
+    sw += w * x[k];
+  }
+  *colsum = su + relax * sw;
+  for (Index k = n - 2; k >= 0; --k) x[k] -= scratch[k + 1] * x[k + 1];
+}
+
 // apply_operator, discretization.hpp:262-278.
 void apply(const Hier& h, int level, const double* u, double* y) {
   const Level& L = h.lv[level];
@@ -163,7 +189,10 @@ void apply(const Hier& h, int level, const double* u, double* y) {
 }
 
 // smooth, relaxation.hpp:63-97 (block_jacobi branch; relax_cell :77-87).
-void smooth(const Hier& h, int level, double* u, const double* f, int sweeps) {
+// rz_col (the fused PCG's finest post-sweep): the last sweep also forms the per-column r.z sums
+// of thomas_rz (f is r there)
+void smooth(const Hier& h, int level, double* u, const double* f, int sweeps,
+            double* rz_col = nullptr) {
   if (!(h.relax > 0.0 && h.relax < 2.0))
     throw Error(E_CONFIG, "smoother relaxation factor must lie in (0, 2)");
   const Level& L = h.lv[level];
@@ -188,8 +217,12 @@ void smooth(const Hier& h, int level, double* u, const double* f, int sweeps) {
       const double* fc = f + T * nr;
       for (Index k = 0; k < nr; ++k) res[k] = fc[k] - res[k];
       try {
-        thomas(nr, col.diag.data(), col.upper.data(), col.lower.data(), res.data(),
-               scratch.data());
+        if (rz_col && s + 1 == sweeps)
+          thomas_rz(nr, col.diag.data(), col.upper.data(), col.lower.data(), res.data(),
+                    scratch.data(), fc, from + T * nr, h.relax, rz_col + T);
+        else
+          thomas(nr, col.diag.data(), col.upper.data(), col.lower.data(), res.data(),
+                 scratch.data());
       } catch (const Error&) {
         failed = true;
         return;
@@ -264,7 +297,7 @@ void prolong(const Hier& h, int coarse_level, const double* coarse, double* fine
 }
 
 // v_cycle, multigrid.hpp:276-299.
-void vcycle(const Hier& h, int level, const double* f, double* u) {
+void vcycle(const Hier& h, int level, const double* f, double* u, double* rz_col = nullptr) {
   const Index nr = h.nz;
   smooth(h, level, u, f, h.nu_pre[level]);
   if (level > 0) {
@@ -279,7 +312,7 @@ void vcycle(const Hier& h, int level, const double* f, double* u) {
     prolong(h, level - 1, uc.data(), pu.data());
     for (Index i = 0; i < n; ++i) u[i] += pu[i];
   }
-  smooth(h, level, u, f, h.nu_post[level]);
+  smooth(h, level, u, f, h.nu_post[level], rz_col);
 }
 
 // Deterministic dot product: sequential sums over 4096-element chunks, then a
@@ -366,6 +399,7 @@ double gridstride_dot(const DevOrder& d, Val val) {
 // descending: the per-column sum runs k = nz-1 .. 0 (sums formed in a back substitution)
 // nc = 2: the two-columns-per-thread smoother (k_jacobi_t4): 64x4 tiles, thread t = (tx, ty)
 // holds columns tx and tx+32 and adds its two column sums before the block tree.
+double column_reduce(const DevOrder& d, const std::vector<double>& colsum, int nc);
 double column_dot(const DevOrder& d, const double* y, const double* u, bool descending = false,
                   int nc = 1) {
   const Index plane = d.plane();
@@ -378,6 +412,12 @@ double column_dot(const DevOrder& d, const double* y, const double* u, bool desc
       for (Index k = 0; k < d.nz; ++k) a += y[c * d.nz + k] * u[c * d.nz + k];
     colsum[c] = a;
   }
+  return column_reduce(d, colsum, nc);
+}
+
+// the per-tile trees of the fused kernels over per-column sums, then k_reduce
+double column_reduce(const DevOrder& d, const std::vector<double>& colsum, int nc) {
+  const Index plane = d.plane();
   std::vector<double> part;
   if (nc == 2) {
     const Index gx = d.nx / 64, gy = d.ny / 4;
@@ -1019,8 +1059,13 @@ int tpmgo_pcg_timed(tpmgo_hier H, const double* f, double* x, double tol, int ma
         return;
       }
       std::fill(z.begin(), z.end(), 0.0);
-      vcycle(h, L, r.data(), z.data());
-      const double rho_new = fused ? column_dot(d, r.data(), z.data(), true, nc) : dotv(r, z);
+      // the fused post-sweep forms r.z in its forward pass (k_jacobi_t3 PCGF 2, thomas_rz); the
+      // two-columns-per-thread kernel sums r_k z_k in its back substitution
+      std::vector<double> rzc(fused && nc == 1 ? h.lv[L].ncells : 0);
+      vcycle(h, L, r.data(), z.data(), rzc.empty() ? nullptr : rzc.data());
+      const double rho_new = fused ? (nc == 1 ? column_reduce(d, rzc, 1)
+                                              : column_dot(d, r.data(), z.data(), true, nc))
+                                   : dotv(r, z);
       if (!(rho_new > 0.0)) {
         *solve_status = BREAKDOWN;
         return;
