@@ -59,6 +59,10 @@ def main():
     print("gap before kernel (top):")
     for k, g in sorted(gk.items(), key=lambda kv: -kv[1])[:10]:
         print(f"  {k:60s} {g / 1e3:.3f} ms")
+    print("largest gaps (predecessor -> successor):")
+    big = sorted(zip(gaps, ev, ev[1:]), key=lambda t: -t[0])[:8]
+    for g, a, b in big:
+        print(f"  {g:8.1f} us  {_name(a)[:45]:45s} -> {_name(b)[:45]}")
 
 
 if __name__ == "__main__":
