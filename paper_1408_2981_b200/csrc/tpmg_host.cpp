@@ -1546,10 +1546,11 @@ int tpmg_pcg(tpmg_hierarchy h, tpmg_field f, tpmg_field x, double tol, int max_i
     *iters = 0;
     *solve_status = TPMG_OK;
     if (r0 == 0.0) return;
-    vcycle(h, L, h->r.p, h->z.p, h->tmp.p, true);
+    // z_0 = M r_0 goes straight into the direction buffer (p_1 = z_0; the first iteration's
+    // V-cycle writes z itself): no 1 GB device copy
+    vcycle(h, L, h->r.p, h->p.p, h->tmp.p, true);
     h->pcur = 0;
-    CUDA_CHECK(cudaMemcpyAsync(h->p.p, h->z.p, n * 8, cudaMemcpyDeviceToDevice, s));
-    dot_into(h, n, h->r.p, h->z.p, 0);
+    dot_into(h, n, h->r.p, h->p.p, 0);
     if (!(read_scalar(h, 0) > 0.0)) {
       *solve_status = TPMG_BREAKDOWN;
       return;
