@@ -196,6 +196,7 @@ struct tpmg_hierarchy_s {
   double* h_scal = nullptr;  // pinned
   bool use_graphs = true;
   bool pcg_fused = false;  // PCG vector work fused into the finest-level smoother sweeps
+  const double* f_first = nullptr;  // fused PCG: the right-hand side the first iteration reads
   bool fuse_rr = true;     // fused residual + transpose restriction (TPMG_FUSE_RR=0 disables)
   // one graph per (iterate buffer, direction parity): key = (const char*)x + pcur
   std::unordered_map<const void*, cudaGraphExec_t> iter_graphs;
@@ -456,8 +457,11 @@ void fill(tpmg_hierarchy h, double* p, int64_t n, double v) {
 //
 // pcg_fuse (finest level of a fused PCG iteration, f == r): the first sweep from zero also does
 // r -= alpha q and |r|^2 (slot 2); the last post-sweep also does r.z (slot 3).
+// f_pre (fused PCG, first iteration): the zero-guess pre-sweep reads the right-hand side from
+// f_pre and writes the updated r to fz.r == f, so r = f_0 never needs a device copy
 void vcycle(tpmg_hierarchy h, int l, const double* f, double* A, double* B, bool zero,
-            bool pcg_fuse = false, const double* p_dir = nullptr) {
+            bool pcg_fuse = false, const double* p_dir = nullptr,
+            const double* f_pre = nullptr) {
   Level& L = h->lv[l];
   const int64_t n = L.plane * h->nz;
   const int npre = h->nu_pre[l], npost = h->nu_post[l], total = npre + npost;
@@ -477,7 +481,7 @@ void vcycle(tpmg_hierarchy h, int l, const double* f, double* A, double* B, bool
     if (npre > 0) {
       // first sweep from zero writes where the last sweep must end in A
       cur = ((total - 1) % 2 == 0) ? A : B;
-      sweep(h, l, nullptr, f, cur, pcg_fuse ? &fz : nullptr, 2);
+      sweep(h, l, nullptr, (pcg_fuse && f_pre) ? f_pre : f, cur, pcg_fuse ? &fz : nullptr, 2);
       s0 = 1;
     } else {
       cur = (npost % 2 == 0) ? A : B;
@@ -580,7 +584,7 @@ void pcg_iteration(tpmg_hierarchy h, double* x, bool first, int pc) {
       }
       apply_level(h, L, tpmg::APPLY_AU, h->pbuf(pc), nullptr, h->q.p, 1);
     }
-    vcycle(h, L, h->r.p, h->z.p, h->tmp.p, true, true);
+    vcycle(h, L, h->r.p, h->z.p, h->tmp.p, true, true, nullptr, first ? h->f_first : nullptr);
     return;
   }
   apply_level(h, L, tpmg::APPLY_AU, h->p.p, nullptr, h->q.p, 1);
@@ -1539,8 +1543,16 @@ int tpmg_pcg(tpmg_hierarchy h, tpmg_field f, tpmg_field x, double tol, int max_i
     const int64_t n = f->buf.n;
     cudaStream_t s = ctx->stream;
     CUDA_CHECK(cudaMemsetAsync(x->buf.p, 0, n * 8, s));
-    CUDA_CHECK(cudaMemcpyAsync(h->r.p, f->buf.p, n * 8, cudaMemcpyDeviceToDevice, s));
-    dot_into(h, n, h->r.p, h->r.p, 2);
+    // r_0 = f.  The fused schedule never copies it: the prologue reads f, and the first
+    // iteration's pre-sweep reads f and writes r_1 = f - alpha q into r (vcycle f_pre)
+    const double* r0p = f->buf.p;
+    if (h->pcg_fused) {
+      h->f_first = f->buf.p;
+    } else {
+      CUDA_CHECK(cudaMemcpyAsync(h->r.p, f->buf.p, n * 8, cudaMemcpyDeviceToDevice, s));
+      r0p = h->r.p;
+    }
+    dot_into(h, n, r0p, r0p, 2);
     const double r0 = std::sqrt(read_scalar(h, 2));
     if (res_hist) res_hist[0] = r0;
     *iters = 0;
@@ -1548,9 +1560,9 @@ int tpmg_pcg(tpmg_hierarchy h, tpmg_field f, tpmg_field x, double tol, int max_i
     if (r0 == 0.0) return;
     // z_0 = M r_0 goes straight into the direction buffer (p_1 = z_0; the first iteration's
     // V-cycle writes z itself): no 1 GB device copy
-    vcycle(h, L, h->r.p, h->p.p, h->tmp.p, true);
+    vcycle(h, L, r0p, h->p.p, h->tmp.p, true);
     h->pcur = 0;
-    dot_into(h, n, h->r.p, h->p.p, 0);
+    dot_into(h, n, r0p, h->p.p, 0);
     if (!(read_scalar(h, 0) > 0.0)) {
       *solve_status = TPMG_BREAKDOWN;
       return;
