@@ -148,7 +148,8 @@ void thomas(Index n, const double* diag, const double* upper, const double* lowe
 // thomas() plus the r.z column sum of the fused finest post-sweep (k_jacobi_t3 PCGF 2):
 // r.z = sum_k r_k u_k + relax sum_k w_k d'_k, with d' the forward pass's values and
 // w_k = r_k - c'_k w_{k-1} (w = U^-T r, U the unit upper factor; c'_0 = 0, w_{-1} = 0), both
-// sums ascending in k; equal to sum_k r_k (u_k + relax x_k) in exact arithmetic.
+// sums ascending in k and every recurrence a fused multiply-add (as the device kernel); equal to
+// sum_k r_k (u_k + relax x_k) in exact arithmetic.
 void thomas_rz(Index n, const double* diag, const double* upper, const double* lower, double* x,
                double* scratch, const double* r, const double* u, double relax, double* colsum) {
   double pivot = diag[0];
@@ -163,9 +164,9 @@ void thomas_rz(Index n, const double* diag, const double* upper, const double* l
   }
   double su = 0.0, sw = 0.0, w = 0.0;
   for (Index k = 0; k < n; ++k) {
-    su += r[k] * u[k];
-    w = r[k] - (k == 0 ? 0.0 : scratch[k]) * w;
-    sw += w * x[k];
+    su = std::fma(r[k], u[k], su);
+    w = std::fma(-(k == 0 ? 0.0 : scratch[k]), w, r[k]);
+    sw = std::fma(w, x[k], sw);
   }
   *colsum = su + relax * sw;
   for (Index k = n - 2; k >= 0; --k) x[k] -= scratch[k + 1] * x[k + 1];
