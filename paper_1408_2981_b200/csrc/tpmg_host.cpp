@@ -195,6 +195,13 @@ struct tpmg_hierarchy_s {
   int* d_err = nullptr;
   double* h_scal = nullptr;  // pinned
   bool use_graphs = true;
+  // Loopback halos (TPMG_LOOPBACK=1 at creation, one rank): every multi-rank device path —
+  // face packing, the send -> recv transfer (here device copies onto this rank itself, the
+  // periodic neighbour of a 1x1 process grid), kernels reading halos from the recv buffers, the
+  // multi-rank schedule (no fused A p / residual+restriction / prolongation) — runs on one GPU,
+  // so the GPU parity tests cover it; only the NCCL transport itself is left out
+  bool loopback = false;
+  bool multi() const;
   bool pcg_fused = false;  // PCG vector work fused into the finest-level smoother sweeps
   const double* f_first = nullptr;  // fused PCG: the right-hand side the first iteration reads
   bool fuse_rr = true;     // fused residual + transpose restriction (TPMG_FUSE_RR=0 disables)
@@ -240,6 +247,8 @@ struct tpmg_hierarchy_s {
     if (h_scal) cudaFreeHost(h_scal);
   }
 };
+
+bool tpmg_hierarchy_s::multi() const { return ctx->world > 1 || loopback; }
 
 struct tpmg_field_s {
   tpmg_hierarchy h = nullptr;
@@ -313,7 +322,8 @@ Halo exchange(tpmg_hierarchy h, int l, const double* u) {
   tpmg_context ctx = h->ctx;
   Level& L = h->lv[l];
   Halo H = tpmg::self_halo(u, L.nx, L.ny, L.plane);
-  if (ctx->world == 1) return H;
+  if (!h->multi()) return H;
+  const bool xs = ctx->px > 1 || h->loopback, ys = ctx->py > 1 || h->loopback;
   const int nz = h->nz;
   const int64_t nwe = (int64_t)L.ny * nz, nsn = (int64_t)L.nx * nz;
   tpmg::launch_pack_faces(ctx->launch(), L.nx, L.ny, nz, u, L.send.p);
@@ -325,6 +335,12 @@ Halo exchange(tpmg_hierarchy h, int l, const double* u) {
   double* rE = rW + nwe;
   double* rS = rE + nwe;
   double* rN = rS + nsn;
+  if (h->loopback) {  // this rank is its own neighbour on every side
+    CUDA_CHECK(cudaMemcpyAsync(rE, sW, nwe * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+    CUDA_CHECK(cudaMemcpyAsync(rW, sE, nwe * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+    CUDA_CHECK(cudaMemcpyAsync(rN, sS, nsn * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+    CUDA_CHECK(cudaMemcpyAsync(rS, sN, nsn * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+  } else {
   NCCL_CHECK(g_nccl.GroupStart());
   if (ctx->px > 1) {
     const int west = ctx->rank_of(ctx->rx - 1, ctx->ry), east = ctx->rank_of(ctx->rx + 1, ctx->ry);
@@ -341,11 +357,12 @@ Halo exchange(tpmg_hierarchy h, int l, const double* u) {
     NCCL_CHECK(g_nccl.Recv(rS, nsn, ncclDouble, south, ctx->comm, ctx->stream));
   }
   NCCL_CHECK(g_nccl.GroupEnd());
-  if (ctx->px > 1) {
+  }
+  if (xs) {
     H.p[0] = rW; H.sk[0] = L.ny; H.st[0] = 1;
     H.p[1] = rE; H.sk[1] = L.ny; H.st[1] = 1;
   }
-  if (ctx->py > 1) {
+  if (ys) {
     H.p[2] = rS; H.sk[2] = L.nx; H.st[2] = 1;
     H.p[3] = rN; H.sk[3] = L.nx; H.st[3] = 1;
   }
@@ -408,7 +425,7 @@ void resid_restrict(tpmg_hierarchy h, int lf, const double* u, const double* f, 
     const Halo H = exchange(h, lf, u);
     tpmg::launch_resid_restrict_sum(h->ctx->launch(), h->vcoef(), F.coef(h->nz), h->xi, u, H, f,
                                     coarse);
-  } else if (h->ctx->world == 1 && h->fuse_rr && tpmg::resid_restrict_T_fusable(F.coef(h->nz))) {
+  } else if (!h->multi() && h->fuse_rr && tpmg::resid_restrict_T_fusable(F.coef(h->nz))) {
     tpmg::launch_resid_restrict_T(h->ctx->launch(), h->vcoef(), F.coef(h->nz), h->xi, u, f,
                                   coarse);
   } else {
@@ -500,7 +517,7 @@ void vcycle(tpmg_hierarchy h, int l, const double* f, double* A, double* B, bool
     Level& C = h->lv[l - 1];
     resid_restrict(h, l, cur, f, C.f.p, other(cur));
     vcycle(h, l - 1, C.f.p, C.u.p, C.t.p, true);
-    fuse_pro = npost > 0 && h->ctx->world == 1 && !h->generic &&
+    fuse_pro = npost > 0 && !h->multi() && !h->generic &&
                h->prolongation == TPMG_PROLONG_LINEAR && tpmg::jacobi_prolong_fusable(L.coef(h->nz));
     if (fuse_pro) {
       pro.ec = C.u.p;
@@ -637,7 +654,7 @@ void run_iteration(tpmg_hierarchy h, double* x, bool first) {
 bool device_loop_ok(tpmg_hierarchy h, int max_iter) {
   const char* e = getenv("TPMG_DEVLOOP");
   const int env = e ? atoi(e) : 0;
-  return env != 0 && h->use_graphs && h->pcg_fused && h->ctx->world == 1 &&
+  return env != 0 && h->use_graphs && h->pcg_fused && !h->multi() &&
          max_iter < tpmg_hierarchy_s::kLoopHist;
 }
 
@@ -878,6 +895,10 @@ int hier_create_impl(tpmg_context ctx, const tpmg_grid_desc* g, const tpmg_facto
 
     auto h = std::make_unique<tpmg_hierarchy_s>();
     h->ctx = ctx;
+    {
+      const char* e = getenv("TPMG_LOOPBACK");
+      h->loopback = ctx->world == 1 && e && atoi(e) != 0;
+    }
     h->nz = (int)nz;
     h->xi = fp ? fp->xi_r != nullptr : (p->xi_r_r != nullptr && p->xi_r_s != nullptr);
     h->cm = cm;
@@ -1094,7 +1115,7 @@ int hier_create_impl(tpmg_context ctx, const tpmg_grid_desc* g, const tpmg_facto
         L.u.alloc(n);
         L.f.alloc(n);
       }
-      if (ctx->world > 1) {
+      if (h->multi()) {
         const int64_t faces = 2 * (int64_t)L.ny * nz + 2 * (int64_t)L.nx * nz;
         L.send.alloc(faces);
         L.recv.alloc(faces);
@@ -1152,7 +1173,7 @@ int hier_create_impl(tpmg_context ctx, const tpmg_grid_desc* g, const tpmg_facto
       // fused direction update + A p (single rank: the halo views of z and p_old are the
       // periodic self views); TPMG_FUSE_AP=0 selects k_pcg_px + the apply kernel
       const char* e3 = getenv("TPMG_FUSE_AP");
-      h->fused_ap = h->pcg_fused && ctx->world == 1 && !(e3 && atoi(e3) == 0) &&
+      h->fused_ap = h->pcg_fused && !h->multi() && !(e3 && atoi(e3) == 0) &&
                     tpmg::pcg_ap_fusable(h->lv[L].coef(h->nz));
       if (h->fused_ap) h->p2.alloc(nf);
       const char* e4 = getenv("TPMG_Q_IN_SWEEP");
