@@ -150,6 +150,7 @@ struct Level {
   DevBuf d_shg;
   DevBuf u, t, f;              // V-cycle work: home iterate, ping-pong partner, rhs
   DevBuf send, recv;           // multi-GPU face buffers [W|E|S|N]
+  DevBuf send2, recv2;         // finest level: a second set (z and p_old before the fused A p)
   DevBuf d_piv, d_cpt;         // coarse levels: pre-factorised column blocks (LevelCoef::piv)
   LevelCoef coef(int nz) const {
     LevelCoef c;
@@ -318,20 +319,22 @@ int plan_levels(int64_t NX, int64_t NY, int px, int py, int depth, bool linear) 
 // Exchange the 1-cell faces of u on level l with the 4 neighbouring ranks and return the
 // view the kernels read across the tile faces.  Dimensions with a single rank wrap onto the
 // tile itself (periodic) without any copy.
-Halo exchange(tpmg_hierarchy h, int l, const double* u) {
+Halo exchange(tpmg_hierarchy h, int l, const double* u, int set = 0) {
   tpmg_context ctx = h->ctx;
   Level& L = h->lv[l];
+  DevBuf& SB = set ? L.send2 : L.send;
+  DevBuf& RB = set ? L.recv2 : L.recv;
   Halo H = tpmg::self_halo(u, L.nx, L.ny, L.plane);
   if (!h->multi()) return H;
   const bool xs = ctx->px > 1 || h->loopback, ys = ctx->py > 1 || h->loopback;
   const int nz = h->nz;
   const int64_t nwe = (int64_t)L.ny * nz, nsn = (int64_t)L.nx * nz;
-  tpmg::launch_pack_faces(ctx->launch(), L.nx, L.ny, nz, u, L.send.p);
-  double* sW = L.send.p;
+  tpmg::launch_pack_faces(ctx->launch(), L.nx, L.ny, nz, u, SB.p);
+  double* sW = SB.p;
   double* sE = sW + nwe;
   double* sS = sE + nwe;
   double* sN = sS + nsn;
-  double* rW = L.recv.p;
+  double* rW = RB.p;
   double* rE = rW + nwe;
   double* rS = rE + nwe;
   double* rN = rS + nsn;
@@ -585,9 +588,10 @@ void pcg_iteration(tpmg_hierarchy h, double* x, bool first, int pc) {
       Level& F = h->lv[L];
       double* po = h->pbuf(pc);
       int nb = 0;
-      tpmg::launch_pcg_ap(ctx->launch(), h->vcoef(), F.coef(h->nz), h->xi, h->z.p,
-                          tpmg::self_halo(h->z.p, F.nx, F.ny, F.plane), po,
-                          tpmg::self_halo(po, F.nx, F.ny, F.plane), h->pbuf(pc ^ 1),
+      // halos of z and p_old (single rank: the periodic self views, no copy)
+      const Halo Hz = exchange(h, L, h->z.p, 0), Hp = exchange(h, L, po, 1);
+      tpmg::launch_pcg_ap(ctx->launch(), h->vcoef(), F.coef(h->nz), h->xi, h->z.p, Hz, po, Hp,
+                          h->pbuf(pc ^ 1),
                           h->q_in_sweep ? nullptr : h->q.p, x, h->scal.p, h->partials.p, &nb);
       tpmg::launch_copy_scalar(ctx->launch(), h->scal.p, 0, 3);
       finish_dot(h, nb, 1);
@@ -1170,12 +1174,18 @@ int hier_create_impl(tpmg_context ctx, const tpmg_grid_desc* g, const tpmg_facto
       // TPMG_FUSE_RR=0 selects the split apply + restrict pair (same bits)
       const char* e2 = getenv("TPMG_FUSE_RR");
       h->fuse_rr = !(e2 && atoi(e2) == 0);
-      // fused direction update + A p (single rank: the halo views of z and p_old are the
+      // fused direction update + A p (halos of z and p_old exchanged first; one rank: the
       // periodic self views); TPMG_FUSE_AP=0 selects k_pcg_px + the apply kernel
       const char* e3 = getenv("TPMG_FUSE_AP");
-      h->fused_ap = h->pcg_fused && !h->multi() && !(e3 && atoi(e3) == 0) &&
+      h->fused_ap = h->pcg_fused && !(e3 && atoi(e3) == 0) &&
                     tpmg::pcg_ap_fusable(h->lv[L].coef(h->nz));
       if (h->fused_ap) h->p2.alloc(nf);
+      if (h->fused_ap && h->multi()) {  // second halo set: z and p_old are exchanged together
+        Level& F = h->lv[L];
+        const int64_t faces = 2 * (int64_t)F.ny * nz + 2 * (int64_t)F.nx * nz;
+        F.send2.alloc(faces);
+        F.recv2.alloc(faces);
+      }
       const char* e4 = getenv("TPMG_Q_IN_SWEEP");
       h->q_in_sweep = h->fused_ap && !(e4 && atoi(e4) == 0);
     }
