@@ -652,9 +652,9 @@ void run_iteration(tpmg_hierarchy h, double* x, bool first) {
   ctx->launches += h->iter_graph_kernels[key];
 }
 
-// Opt-in (TPMG_DEVLOOP=1, read per solve): measured no faster than the host loop once its
-// per-iteration synchronisation was reduced to one, and ncu does not profile kernels inside
-// conditional graph bodies, so the evidence pipeline keeps the host loop by default.
+// Opt-in (TPMG_DEVLOOP=1, read per solve): bench.py measures the same solve time either way
+// (24.9 GDOF/s) once the host loop synchronises once per iteration, and ncu does not profile
+// kernels inside conditional graph bodies, so the host loop stays the default.
 bool device_loop_ok(tpmg_hierarchy h, int max_iter) {
   const char* e = getenv("TPMG_DEVLOOP");
   const int env = e ? atoi(e) : 0;

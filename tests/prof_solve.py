@@ -4,6 +4,9 @@ box for the per-launch list.  Not a pytest file."""
 import os
 import sys
 
+# ncu / CUPTI do not see kernels inside conditional graph bodies: profile the host PCG loop
+os.environ.setdefault("TPMG_DEVLOOP", "0")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_1408_2981_b200 import synth, tpmg  # noqa: E402

@@ -8,6 +8,9 @@ import collections
 import os
 import sys
 
+# ncu / CUPTI do not see kernels inside conditional graph bodies: profile the host PCG loop
+os.environ.setdefault("TPMG_DEVLOOP", "0")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import torch  # noqa: E402
