@@ -350,3 +350,33 @@ def test_synthetic_rhs_mean_removed_and_decomposition_independent():
     assert synth.mean_from_m_sum(sum(parts), 32 * 16 * 8) == mean
     t2 = synth.rhs_x_fastest(0, 32, 16, 8, x0=16, y0=8, lnx=16, lny=8, mean=mean)
     assert np.array_equal(t2, tile)
+
+
+@pytest.mark.parametrize("cfg", ["cfg1", "small_graded"])
+def test_forward_pass_rz_matches_direct_dot(O, cfg):
+    """The fused schedule's r.z (sum r u + relax sum w d' with w = U^-T r, formed in the
+    post-sweep's forward pass; oracle thomas_rz) against the plain schedule's direct r.z dot:
+    the same PCG to rounding.  A CG residual history is only reproducible to the rounding of its
+    dot products: merely reordering the direct dots (device tree vs host chunks) moves it by up
+    to ~4e-9 on the 33-iteration problem, so the reformulation must stay within that envelope
+    (and the product matches the oracle's own formula bit for bit)."""
+    P = (synth.baseline_config(1) if cfg == "cfg1" else
+         synth.make_problem(64, 32, 16, omega2=1e-3, lambda2=1e-4, grading="quadratic",
+                            profile="uniform", profile_seed=3, depth=3, name=cfg))
+    f = synth.x_fastest_to_k_fastest(P.rhs())
+
+    def run(fused, device_order=True):
+        h = O.OracleHierarchy.from_problem(P)
+        O.lib().tpmgo_set_pcg_fused(h._h, fused)
+        h.set_device_order(device_order)
+        return h.pcg(f, P.tol, 200)
+
+    x1, h1, it1, s1 = run(1)
+    x0, h0, it0, s0 = run(0)
+    _, h0h, it0h, _ = run(0, device_order=False)  # the same dots, another summation order
+    assert s1 == s0 == 0 and it1 == it0 == it0h
+    d_formula = np.max(np.abs(h1 - h0) / h0)
+    d_order = np.max(np.abs(h0h - h0) / h0)
+    assert d_formula <= max(2.0 * d_order, 1e-13), (d_formula, d_order)
+    assert d_formula <= 1e-8
+    assert np.max(np.abs(x1 - x0)) <= 1e-8 * np.max(np.abs(x0))
