@@ -1,3 +1,6 @@
+# A/B solve timing on the GPU box (profiling helper): one config-3 hierarchy per argument, the
+# argument being the TPMG_L2HINT value; other TPMG_* variables pass through from the caller.
+# Prints min / median of 5 solves after 2 warm-up solves.  Usage: bash tests/solve_ab.sh 1 1
 for h in "$@"; do TPMG_L2HINT=$h timeout 300 python -c "
 import sys,time; sys.path.insert(0,'.')
 from paper_1408_2981_b200 import synth, tpmg
