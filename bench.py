@@ -101,11 +101,10 @@ def dist_env():
 
 
 def proc_grid(n: int):
-    px = 1
-    while px * px < n:
-        px *= 2
-    px = min(px, n)
-    return px, n // px  # 1->(1,1) 2->(2,1) 4->(2,2) 8->(4,2)
+    """px x py = n with py the largest divisor of n not above sqrt(n):
+    1->(1,1) 2->(2,1) 3->(3,1) 4->(2,2) 6->(3,2) 8->(4,2)."""
+    py = max(d for d in range(1, int(math.isqrt(n)) + 1) if n % d == 0)
+    return n // py, py
 
 
 def make_problem(px: int, py: int):

@@ -65,8 +65,12 @@ def build_oracle(force: bool = False) -> str:
 
 
 def build_all(force: bool = False, verbose: bool = False):
-    paths = [build_lib("exact", force, verbose), build_lib("fma", force, verbose), build_oracle(force)]
-    return paths
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(3) as ex:  # nvcc runs are independent processes
+        jobs = [ex.submit(build_lib, "exact", force, verbose), ex.submit(build_lib, "fma", force, verbose),
+                ex.submit(build_oracle, force)]
+        return [j.result() for j in jobs]
 
 
 if __name__ == "__main__":

@@ -544,12 +544,17 @@ void vcycle(tpmg_hierarchy h, int l, const double* f, double* A, double* B, bool
 void sync_check(tpmg_hierarchy h) {
   // the error flag rides behind the queued work into pinned memory: one synchronisation
   int* h_err = reinterpret_cast<int*>(h->h_scal + 7);
+  // multi-rank: every rank must take the same exit decision, or the ranks that did not see a
+  // zero pivot would enter the next iteration's collectives alone and hang
+  if (h->ctx->world > 1)
+    NCCL_CHECK(g_nccl.AllReduce(h->d_err, h->d_err, 1, ncclInt32, ncclMax, h->ctx->comm,
+                                h->ctx->stream));
   CUDA_CHECK(cudaMemcpyAsync(h_err, h->d_err, sizeof(int), cudaMemcpyDeviceToHost,
                              h->ctx->stream));
   CUDA_CHECK(cudaStreamSynchronize(h->ctx->stream));
   const int err = *h_err;
   if (err) {
-    CUDA_CHECK(cudaMemset(h->d_err, 0, sizeof(int)));
+    CUDA_CHECK(cudaMemsetAsync(h->d_err, 0, sizeof(int), h->ctx->stream));
     throw Error(TPMG_E_SINGULAR, "thomas_solve: zero pivot");
   }
 }
@@ -1132,9 +1137,9 @@ int hier_create_impl(tpmg_context ctx, const tpmg_grid_desc* g, const tpmg_facto
     h->r.alloc(nf); h->z.alloc(nf); h->p.alloc(nf); h->q.alloc(nf); h->tmp.alloc(nf);
     h->partials.alloc(std::max<int64_t>(max_blocks, 148 * 8));
     h->scal.alloc(8);
-    CUDA_CHECK(cudaMemset(h->scal.p, 0, 8 * sizeof(double)));
+    CUDA_CHECK(cudaMemsetAsync(h->scal.p, 0, 8 * sizeof(double), h->ctx->stream));
     CUDA_CHECK(cudaMalloc(&h->d_err, sizeof(int)));
-    CUDA_CHECK(cudaMemset(h->d_err, 0, sizeof(int)));
+    CUDA_CHECK(cudaMemsetAsync(h->d_err, 0, sizeof(int), h->ctx->stream));
     CUDA_CHECK(cudaMallocHost(&h->h_scal, 8 * sizeof(double)));
     // Coarse levels (the warp-per-column regime, L2 resident): the column blocks' Thomas
     // factorisation is formed once here, so their sweeps only carry the right-hand side through
@@ -1162,7 +1167,7 @@ int hier_create_impl(tpmg_context ctx, const tpmg_grid_desc* g, const tpmg_facto
           L.d_cpt.reset();
         }
       }
-      CUDA_CHECK(cudaMemset(h->d_err, 0, sizeof(int)));
+      CUDA_CHECK(cudaMemsetAsync(h->d_err, 0, sizeof(int), h->ctx->stream));
     }
     {
       const int L = levels - 1;
@@ -1252,7 +1257,10 @@ int tpmg_hier_create_generic(tpmg_context ctx, int n_levels, int nz, int nnb, in
     for (int j = 0; j < nchild; ++j) {
       h->rule.d1[j] = prol_d1 ? prol_d1[j] : -1;
       h->rule.d2[j] = prol_d2 ? prol_d2[j] : -1;
-      if (n_levels > 1 && h->rule.d1[j] >= nnb) throw Error(TPMG_E_CONFIG, "prolongation rule out of range");
+      // d1 = -1: centre child (= parent); otherwise two neighbour slots of the parent
+      if (n_levels > 1 && (h->rule.d1[j] < -1 || h->rule.d1[j] >= nnb ||
+                           (h->rule.d1[j] >= 0 && (h->rule.d2[j] < 0 || h->rule.d2[j] >= nnb))))
+        throw Error(TPMG_E_CONFIG, "prolongation rule out of range");
     }
     check_finite(bv, nz, "bv"); check_finite(sv, nz, "sv");
     check_finite(av, nz + 1, "av"); check_finite(xv, nz + 1, "xv");
@@ -1300,9 +1308,9 @@ int tpmg_hier_create_generic(tpmg_context ctx, int n_levels, int nz, int nnb, in
     h->r.alloc(nf); h->z.alloc(nf); h->p.alloc(nf); h->q.alloc(nf); h->tmp.alloc(nf);
     h->partials.alloc(std::max<int64_t>(max_blocks, 148 * 8));
     h->scal.alloc(8);
-    CUDA_CHECK(cudaMemset(h->scal.p, 0, 8 * sizeof(double)));
+    CUDA_CHECK(cudaMemsetAsync(h->scal.p, 0, 8 * sizeof(double), h->ctx->stream));
     CUDA_CHECK(cudaMalloc(&h->d_err, sizeof(int)));
-    CUDA_CHECK(cudaMemset(h->d_err, 0, sizeof(int)));
+    CUDA_CHECK(cudaMemsetAsync(h->d_err, 0, sizeof(int), h->ctx->stream));
     CUDA_CHECK(cudaMallocHost(&h->h_scal, 8 * sizeof(double)));
     *out = h.release();
   });
@@ -1600,7 +1608,7 @@ int tpmg_pcg(tpmg_hierarchy h, tpmg_field f, tpmg_field x, double tol, int max_i
     }
     // fused schedule: the last iteration's x += alpha p is still pending when the loop ends
     auto finish_x = [&] {
-      if (h->pcg_fused) {
+      if (h->pcg_fused && *iters > 0) {  // max_iter = 0: no pending update, x stays 0
         tpmg::launch_pcg_xfinal(ctx->launch(), n, h->scal.p, h->pbuf(h->pcur), x->buf.p);
         sync_check(h);
       }

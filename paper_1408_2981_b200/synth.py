@@ -295,3 +295,18 @@ def baseline_config(i: int, **over) -> Problem:
     kw.update(over)
     nx, ny, nz = kw.pop("nx"), kw.pop("ny"), kw.pop("nz")
     return make_problem(nx, ny, nz, **kw)
+
+
+def parity_problem(name: str) -> Problem:
+    """The solves pinned by oracle goldens at BASELINE.json's stated sizes
+    (tests/golden/oracle_<name>_pcg.json, made by tests/golden/make_golden_large.py)."""
+    if name == "cfg2":
+        return baseline_config(2)
+    if name == "cfg3":
+        return baseline_config(3)
+    if name == "cfg4s":  # config 4's strong-scaling problem: 9 levels to a global 8x8
+        return baseline_config(3, nx=2048, ny=2048, depth=9, name="cfg4s_2048x2048x128")
+    if name == "cfg5t":  # a 2048^2 tile of config 5 (its h = 1/4096), 9 levels to 8x8
+        return baseline_config(5, nx=2048, ny=2048, depth=9, h=1.0 / 4096,
+                               name="cfg5t_2048x2048x64")
+    raise ValueError(f"unknown parity problem {name!r}")
