@@ -1,15 +1,24 @@
 #!/usr/bin/env python
-"""Headline benchmark: PCG + TPMG V(1,1) solve of BASELINE.json config 3 (1024x1024x128,
-fp64) on the sm_100a path, one process per GPU.
+"""Headline benchmark: the PCG + TPMG solve of BASELINE.json on the sm_100a path, one process
+per GPU.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 3|4w|4s|5]
 
-One STEP = one complete PCG solve (x0 = 0 -> |r|/|r0| <= 1e-8) of the synthetic problem.
-N = 1: config 3.  N > 1 (torchrun): weak scaling, a (1024*px) x (1024*py) x 128 global grid,
-1024^2 x 128 columns per GPU, decomposed horizontally (columns never split).
+One STEP = one complete PCG solve (x0 = 0 -> |r|/|r0| <= tol) of the synthetic problem.
+--config (BASELINE.json configs; seeded synthetic inputs of their shapes, no dataset exists):
+  3   (default, N = 1)  config 3: 1024^2 x 128, V(1,1), 8 levels to 8x8, tol 1e-8
+  4w  (default, N > 1)  config 4 weak scaling: 1024^2 x 128 per GPU, (1024 px) x (1024 py)
+                        global, each GPU's tile coarsened to 8x8
+  4s                    config 4 strong scaling: 2048^2 x 128 global on N GPUs, 9 levels to a
+                        global 8x8
+  5                     config 5: 4096^2 x 64, omega^2 = 1e-5, lambda^2 = 1e-6, lognormal
+                        profile, geometric grading 1.1, V(2,2), tol 1e-10, 10 levels
 value = whole-job throughput in GDOF/s = global DOF x PCG iterations / second (max over
-ranks).  Extra keys give PCG iterations/s, V-cycle GDOF/s, the roofline of the dominant
-kernel (line-Jacobi sweep) and the CPU baseline (the oracle port on the host cores).
+ranks).  The line also carries PCG iterations/s, V-cycle GDOF/s, live per-launch durations of
+the finest-level kernels inside the timed solves (CUDA event probes in the iteration graph),
+the roofline of the one with the largest share of the solve, parity against the committed
+oracle golden of the same solve, and the CPU baseline (the oracle port on the host cores).
 --impl reference times the CPU restatement of the reference path (oracle/) on the host.
 """
 from __future__ import annotations
@@ -107,20 +116,57 @@ def proc_grid(n: int):
     return n // py, py
 
 
-def make_problem(px: int, py: int):
+def make_problem(cfg: str, px: int, py: int):
+    """(problem, workload name, scaling, parity golden name or None)."""
     from paper_1408_2981_b200 import synth
 
-    if px * py == 1:
-        return synth.baseline_config(3)
-    # config 4 (weak): 1024^2 x 128 per GPU, same h, operator and RHS distribution
-    return synth.make_problem(
-        1024 * px, 1024 * py, 128, omega2=1e-3, lambda2=1e-4, grading="quadratic", depth=8,
-        nu=1, tol=1e-8, h=1.0 / 1024, name=f"cfg4_weak_{px}x{py}")
+    n = px * py
+    if cfg == "3" and n > 1:
+        cfg = "4w"
+    if cfg == "3":
+        return synth.baseline_config(3), "config 3 (1 GPU solve)", "weak", "cfg3"
+    if cfg == "4w":  # 1024^2 x 128 per GPU, same h, operator and RHS distribution
+        P = synth.make_problem(
+            1024 * px, 1024 * py, 128, omega2=1e-3, lambda2=1e-4, grading="quadratic", depth=8,
+            nu=1, tol=1e-8, h=1.0 / 1024, name=f"cfg4w_{1024 * px}x{1024 * py}x128")
+        return P, f"config 4 weak scaling ({px}x{py} GPUs)", "weak", "cfg3" if n == 1 else None
+    if cfg == "4s":
+        return (synth.parity_problem("cfg4s"), f"config 4 strong scaling ({px}x{py} GPUs)",
+                "strong", "cfg4s" if n == 1 else None)
+    if cfg == "5":
+        return synth.baseline_config(5), f"config 5 ({px}x{py} GPUs)", "strong", None
+    raise SystemExit(f"unknown --config {cfg}")
+
+
+def config_dict(P, workload: str, px: int, py: int, levels=None) -> dict:
+    """The one config dict both arms print (same workload, same keys)."""
+    return {"workload": f"{P.name}: {workload}", "global_grid": [P.nx, P.ny, P.nz],
+            "tile": [P.nx // px, P.ny // py, P.nz], "process_grid": [px, py],
+            "solver": f"PCG + TPMG V({P.nu_pre},{P.nu_post}), block line-Jacobi relax={P.relax}, "
+                      f"{'linear' if P.prolongation == 0 else 'injection'} prolongation + "
+                      f"{'transpose' if P.restriction == 1 else 'summation'} restriction, "
+                      f"coarsest level 1 sweep",
+            "tol": P.tol, "levels": levels if levels is not None else P.depth,
+            "omega2": P.omega ** 2, "lambda2": float(P.beta_r[0]),
+            "l2": "inputs larger than L2 (one field >= 1.07 GB)"}
+
+
+def load_golden(name):
+    if name is None:
+        return None
+    path = os.path.join(ROOT, "tests", "golden", f"oracle_{name}_pcg.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as fh:
+        g = json.load(fh)
+    g["path"] = os.path.relpath(path, ROOT)
+    return g
 
 
 class CpuPort:
-    """The oracle port (the reference's algorithm, parallel_for threading) on the host cores:
-    seconds per PCG iteration from the solve's ConvergenceHistory seconds column."""
+    """The oracle port (the reference's algorithm, parallel_for threading) on the host cores.
+    One sample = r0, the prologue V-cycle and `iters` PCG iterations of the same solve; its
+    step time is the iterations' span from the solve's ConvergenceHistory seconds column."""
 
     def __init__(self, P, threads: int):
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -134,39 +180,50 @@ class CpuPort:
         self.f = synth.x_fastest_to_k_fastest(P.rhs())
 
     def sample(self, iters: int = 2):
+        """seconds of `iters` PCG iterations (prologue excluded)."""
         _, hist, it, st, secs = self.o.pcg(self.f, self.P.tol, iters, seconds=True)
-        return (secs[it] - secs[1]) / max(it - 1, 1) if it >= 2 else secs[it]
+        return secs[it] - secs[0], it
 
 
-def cpu_port_sample(P, threads: int, iters: int = 2):
-    return CpuPort(P, threads).sample(iters), iters
+def cpu_sample_problem(P):
+    """The CPU leg's workload: the same problem, or a 2048^2 tile of config 5 (its 4096^2 x 64
+    grid needs ~80 GB on the host)."""
+    from paper_1408_2981_b200 import synth
+
+    if P.nx * P.ny * P.nz > 2048 * 2048 * 128:
+        return synth.parity_problem("cfg5t"), "a 2048^2 x 64 tile of config 5 (same h, operator)"
+    return P, "the same problem"
 
 
 def run_reference(args):
     """--impl reference: the CPU restatement of the reference path (oracle port), all host
-    threads, bounded sample per step (2 PCG iterations of the same config)."""
+    threads; one step = 2 PCG iterations of the same solve (bounded sample)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    P = make_problem(*proc_grid(world))
+    px, py = proc_grid(world)
+    P, workload, scaling, _ = make_problem(args.config, px, py)
+    Q, what = cpu_sample_problem(P)
     threads = os.cpu_count() or 1
-    port = CpuPort(P, threads)
-    per = []
+    port = CpuPort(Q, threads)
+    per, its = [], 2
     for s in range(args.warmup + args.steps):
-        t = port.sample(iters=2)
+        t, its = port.sample(iters=2)
         if s >= args.warmup:
             per.append(t)
-    t_iter = statistics.median(per)
-    value = P.n_dof / t_iter / 1e9
+    t_step = statistics.median(per)
+    value = Q.n_dof * its / t_step / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GDOF/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t_iter * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE configs)",
-        "config": {"workload": P.name, "nx": P.nx, "ny": P.ny, "nz": P.nz, "sample": "per step: 2 PCG iterations"},
-        "pcg_iterations_per_s": 1.0 / t_iter,
+        "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": scaling,
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded counter-based RNG, BASELINE.json config shapes)",
+        "config": config_dict(P, workload, px, py),
+        "pcg_iterations_per_s": its / t_step,
         "cpu_baseline": {"value": value, "unit": "GDOF/s", "cores": threads, "kind": "port",
-                         "sample": f"{P.name}: PCG iterations 2.. of an oracle solve, per-iteration time"},
+                         "sample": f"{Q.name} ({what}): per step {its} PCG iterations of an "
+                                   f"oracle solve (after r0 and the prologue V-cycle)"},
         "e2e": {"value": value, "unit": "GDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -179,12 +236,15 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="3", choices=["3", "4w", "4s", "5"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--max-iter", type=int, default=500)
     ap.add_argument("--no-coef", action="store_true", help="skip the coefficient-storage comparison")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+
+    import hashlib
 
     import numpy as np
     import torch
@@ -196,7 +256,7 @@ def main():
     if world > 1:
         dist.init_process_group("gloo", init_method="env://")
     px, py = proc_grid(world)
-    P = make_problem(px, py)
+    P, workload, scaling, golden_name = make_problem(args.config, px, py)
     torch.cuda.set_device(local)
 
     nccl_id = None
@@ -230,13 +290,17 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    # live kernel probes: CUDA event pairs around the finest-level PCG kernels, recorded into
+    # the iteration graph (captured during the warm-up)
+    h.kernel_probe(True)
     # ---- warm-up ------------------------------------------------------------------------------
     res = None
     for _ in range(args.warmup):
         res = tpmg.pcg_solve(h, f, x, P.tol, args.max_iter)
+    h.kernel_probe(True)  # resets the totals (the graphs captured with probes are kept)
     # ---- timed region: K solves, device time by CUDA events on the library stream -------------
     launches0 = ctx.kernel_launches()
-    iters = []
+    iters, hists = [], []
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -245,6 +309,7 @@ def main():
         for _ in range(args.steps):
             res = tpmg.pcg_solve(h, f, x, P.tol, args.max_iter)
             iters.append(res.iterations)
+            hists.append(res.history)
         e1.record(stream)
         e1.synchronize()
     torch.cuda.synchronize()
@@ -256,22 +321,53 @@ def main():
     it_per_s = total_iters / (ms / 1e3)
     value = P.n_dof * it_per_s / 1e9
 
-    # ---- e2e: the same solve through the public API from pinned host memory ---------------------
+    # ---- live per-launch durations of the finest-level kernels in the timed solves -------------
+    peak, peak_kind = _peaks()
     n_local = lnx * lny * nz
-    f_pin = torch.from_numpy(f_host.reshape(-1)).pin_memory()
+    C_cols, N_dof = lnx * lny, n_local
+    # algorithmic bytes per launch: fields read + written once, 2 B/DOF for a
+    # quarter-size coarse field, 32 B per column of hatted scalars
+    live_defs = (("pcg_direction_Ap", tpmg.K_PCG_DIRECTION, 40 * N_dof + 32 * C_cols,
+                  "k_pcg_ap: x += a p_old; p = z + b p_old; A p, p.(A p)"),
+                 ("pcg_rupdate_presweep", tpmg.K_PCG_RUPDATE, 32 * N_dof + 32 * C_cols,
+                  "k_jacobi_t3 PCGF=3: q = A p re-formed, r -= a q, |r|^2, sweep from zero"),
+                 ("pcg_postsweep_rz", tpmg.K_PCG_POSTSWEEP, 24 * N_dof + 32 * C_cols,
+                  "k_jacobi_t3 PCGF=2: line-Jacobi sweep + r.z partials"),
+                 ("resid_restrict", tpmg.K_RESID_RESTRICT, 18 * N_dof + 32 * C_cols,
+                  "k_resid_restrict_T2: coarse = P^T (f - A u)"),
+                 ("prolong_add", tpmg.K_PROLONG_ADD, 18 * N_dof,
+                  "k_prolong_flat: u += P e"))
+    kernels_live = {}
+    for name, kid, by, what in live_defs:
+        tot, n = h.kernel_probe_read(kid)
+        tot, n = max_over_ranks(tot), n
+        if n == 0:
+            continue
+        avg = tot / n
+        kernels_live[name] = {"kernel": what, "launches": n, "avg_ms": avg,
+                              "share_of_timed_region": tot / ms, "algorithmic_bytes": by,
+                              "GBps": by / (avg * 1e-3) / 1e9,
+                              "frac": by / (avg * 1e-3) / 1e9 / peak}
+    h.kernel_probe(False)
+    top = max(kernels_live, key=lambda k: kernels_live[k]["share_of_timed_region"]) if kernels_live else None
+
+    # ---- e2e: the same solve through the public API, host buffers in the reference's k-fastest
+    # Field order (permutation kernels at the boundary), pinned host memory -------------------------
+    f_k = synth.x_fastest_to_k_fastest(f_host)
+    f_pin = torch.from_numpy(f_k.reshape(-1)).pin_memory()
     x_pin = torch.empty(n_local, dtype=torch.float64).pin_memory()
     fnp, xnp = f_pin.numpy(), x_pin.numpy()
     ef = h.field()
-    tpmg.pcg_solve(h, ef.upload(fnp), x, P.tol, args.max_iter)  # warm
+    tpmg.pcg_solve(h, ef.upload(fnp, layout=tpmg.K_FASTEST), x, P.tol, args.max_iter)  # warm
     barrier()
     torch.cuda.synchronize()
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2e_iters = 0
     e2.record(stream)
     for _ in range(args.steps):
-        ef.upload(fnp)
+        ef.upload(fnp, layout=tpmg.K_FASTEST)
         r2 = tpmg.pcg_solve(h, ef, x, P.tol, args.max_iter)
-        x.download(out=xnp)
+        x.download(layout=tpmg.K_FASTEST, out=xnp)
         e2e_iters += r2.iterations
     e3.record(stream)
     e3.synchronize()
@@ -279,23 +375,36 @@ def main():
     e2e_ms = max_over_ranks(e2.elapsed_time(e3))
     e2e_value = P.n_dof * e2e_iters / (e2e_ms / 1e3) / 1e9
 
-    # ---- dominant kernel roofline (live CUDA-event timing on the library stream) -----------------
-    peak, peak_kind = _peaks()
-    C_cols, N_dof = lnx * lny, n_local
-    t_jac = h.time_kernel(tpmg.K_JACOBI, h.finest, reps=20)
-    jac_bytes = 24 * N_dof + 32 * C_cols  # read u, f; write u'; 4 per-column scalars
-    achieved = jac_bytes / (t_jac * 1e-3) / 1e9
-    kernels = {}
-    # algorithmic bytes: fields read + written once, 2 B/DOF for a quarter-size coarse field,
-    # 32 B per column of hatted scalars
-    for name, kid, by in (("pcg_direction_Ap", tpmg.K_PCG_DIRECTION, 40 * N_dof + 32 * C_cols),
-                          ("pcg_rupdate_presweep", tpmg.K_PCG_RUPDATE, 32 * N_dof + 32 * C_cols),
+    # ---- parity: the timed solves against the committed oracle golden of the same solve ------
+    parity = None
+    g = load_golden(golden_name) if world == 1 else None
+    if g is not None:
+        hist_o = np.array([float.fromhex(v) for v in g["history_hex"]])
+        n = min(len(hist_o), len(res.history))
+        rel = float(np.max(np.abs(res.history[:n] - hist_o[:n]) / hist_o[:n]))
+        xs = x.download()
+        parity = {"golden": g["path"], "iterations": res.iterations,
+                  "oracle_iterations": g["iterations"],
+                  "history_max_rel_diff": rel,
+                  "history_bitwise": [float(v).hex() for v in res.history] == g["history_hex"],
+                  "all_timed_solves_identical": all(
+                      len(hh) == len(res.history) and bool(np.all(hh == res.history)) for hh in hists),
+                  "iterate_sha256_match": hashlib.sha256(
+                      np.ascontiguousarray(xs, dtype="<f8").tobytes()).hexdigest()
+                      == g["x_sha256_device_order"],
+                  "north_star_bar": "history <= 1e-10 relative, iterations +-1",
+                  "pass": rel <= 1e-10 and abs(res.iterations - g["iterations"]) <= 1}
+    elif world > 1:
+        parity = {"note": "multi-GPU solves only change the all-reduce order; checked on one GPU "
+                          "against the goldens (tests/test_gpu_parity_large.py)"}
+
+    # ---- standalone kernel timings (scratch operands, back-to-back launches) ------------------
+    standalone = {}
+    for name, kid, by in (("jacobi", tpmg.K_JACOBI, 24 * N_dof + 32 * C_cols),
                           ("jacobi_zero_guess", tpmg.K_JACOBI_ZERO, 16 * N_dof + 32 * C_cols),
-                          ("resid_restrict", tpmg.K_RESID_RESTRICT, 16 * N_dof + 2 * N_dof + 32 * C_cols),
-                          ("prolong_add", tpmg.K_PROLONG_ADD, 16 * N_dof + 2 * N_dof),
                           ("apply", tpmg.K_APPLY, 16 * N_dof + 32 * C_cols)):
         t = h.time_kernel(kid, h.finest, reps=10)
-        kernels[name] = {"ms": t, "GBps": by / (t * 1e-3) / 1e9, "frac": by / (t * 1e-3) / 1e9 / peak}
+        standalone[name] = {"ms": t, "GBps": by / (t * 1e-3) / 1e9, "frac": by / (t * 1e-3) / 1e9 / peak}
     # V-cycle alone
     vz = h.field()
     torch.cuda.synchronize()
@@ -307,12 +416,13 @@ def main():
     e5.record(stream)
     e5.synchronize()
     vcycle_ms = e4.elapsed_time(e5) / 5
+    del vz, ef
 
     # ---- coefficient storage trade-off (PAPER's TPMG(full) vs
     # TPMG(partial) vs tensor-product): the same PCG solve with partial and full (dense) hatted
     # coefficients, at BASELINE config 2's size so that the default run stays short -----------
     coef_modes = None
-    if world == 1 and not args.no_coef:
+    if world == 1 and not args.no_coef and args.config == "3":
         P2 = synth.baseline_config(2)
         coef_modes = {"workload": f"{P2.name}: PCG + V(1,1) to 1e-8, one warm and one timed solve",
                       "coef_bytes_per_dof": {"factorized": 0, "partial": 8, "full": 48}}
@@ -336,46 +446,55 @@ def main():
             h2.close()
 
     traffic = None
-    prof_json = os.path.join(ROOT, "profiles", "jacobi_traffic.json")
-    if os.path.exists(prof_json):
+    prof_json = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+    if os.path.exists(prof_json) and top is not None:
         try:
             with open(prof_json) as fh:
-                traffic = json.load(fh).get("dram_bytes_per_launch")
+                traffic = json.load(fh).get(top, {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
+
+    roofline = None
+    if top is not None:
+        k = kernels_live[top]
+        roofline = {"bound": "hbm", "kernel": f"{k['kernel']} (finest level; largest share of "
+                                              f"the timed solves)",
+                    "achieved": k["GBps"], "peak": peak, "unit": "GB/s", "frac": k["frac"],
+                    "traffic": traffic, "algorithmic_bytes": k["algorithmic_bytes"],
+                    "launch_ms": k["avg_ms"], "launches_timed": k["launches"],
+                    "timing": "CUDA events around each launch inside the timed solves "
+                              "(library stream, graph event nodes)",
+                    "peak_kind": peak_kind}
 
     line = {
         "metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded counter-based RNG, BASELINE.json config shapes)",
-        "config": {"workload": P.name + (" (config 3)" if world == 1 else " (config 4 weak)"),
-                   "global_grid": [P.nx, P.ny, P.nz], "tile": [lnx, lny, nz],
-                   "solver": "PCG + TPMG V(1,1), line-Jacobi, linear/transpose transfers",
-                   "tol": P.tol, "levels": h.n_levels, "process_grid": [px, py],
-                   "l2": "inputs larger than L2 (1.07 GB per vector)"},
+        "config": config_dict(P, workload, px, py, h.n_levels),
         "pcg_iterations_per_s": it_per_s, "pcg_iterations_per_solve": iters,
         "vcycle_gdof_per_s": N_dof / (vcycle_ms * 1e-3) / 1e9, "vcycle_ms": vcycle_ms,
         "gpu_launches": launches,
-        "roofline": {"bound": "hbm", "kernel": "k_jacobi (line-Jacobi sweep, finest level)",
-                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "algorithmic_bytes": jac_bytes, "launch_ms": t_jac,
-                     "peak_kind": peak_kind},
-        "kernels": kernels,
+        "roofline": roofline,
+        "kernels_live": kernels_live,
+        "kernels_standalone": standalone,
+        "parity": parity,
         "coef_modes": coef_modes,
         "e2e": {"value": e2e_value, "unit": "GDOF/s", "h2d_bytes_per_step": 8 * n_local,
-                "d2h_bytes_per_step": 8 * n_local, "ms_per_step": e2e_ms / args.steps},
+                "d2h_bytes_per_step": 8 * n_local, "ms_per_step": e2e_ms / args.steps,
+                "layout": "host buffers in the reference's k-fastest Field order (pinned)"},
         "clocks": clk.summary(),
     }
     # ---- CPU baseline: oracle port on the host cores (rank 0, N = 1 only) -----------------------
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             threads = os.cpu_count() or 1
-            t_cpu, _ = cpu_port_sample(P, threads, iters=2)
-            line["cpu_baseline"] = {"value": P.n_dof / t_cpu / 1e9, "unit": "GDOF/s",
+            Q, what = cpu_sample_problem(P)
+            t_cpu, its = CpuPort(Q, threads).sample(iters=2)
+            line["cpu_baseline"] = {"value": Q.n_dof * its / t_cpu / 1e9, "unit": "GDOF/s",
                                     "cores": threads, "kind": "port",
-                                    "sample": f"{P.name}: PCG iteration 2 of an oracle solve "
-                                              f"({t_cpu:.2f} s/iteration)"}
+                                    "sample": f"{Q.name} ({what}): {its} PCG iterations of an "
+                                              f"oracle solve ({t_cpu / its:.2f} s/iteration)"}
         except Exception as e:  # noqa: BLE001
             line["cpu_baseline"] = {"value": None, "unit": "GDOF/s", "cores": 0, "kind": "port",
                                     "sample": f"failed: {e}"}

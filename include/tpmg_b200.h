@@ -362,12 +362,21 @@ typedef enum tpmg_kernel_id {
   TPMG_K_RESTRICT = 5,        /* coarse = R fine                          */
   TPMG_K_RESIDUAL = 6,        /* r = f - A u                              */
   TPMG_K_PCG_DIRECTION = 7,   /* fused PCG pass: x += a p; p = z + b p; A p and p.(A p) */
-  TPMG_K_PCG_RUPDATE = 8      /* fused PCG pre-sweep: r -= a A p, |r|^2, z = smoother(r) */
+  TPMG_K_PCG_RUPDATE = 8,     /* fused PCG pre-sweep: r -= a A p, |r|^2, z = smoother(r) */
+  TPMG_K_PCG_POSTSWEEP = 9    /* fused PCG post-sweep: z = smoother(u) and the r.z partials */
 } tpmg_kernel_id;
 /* Average device time (CUDA events on the library's stream) of `reps` back-to-back launches
  * of one hot-path kernel on `level` (transfers: `level` is the fine level), on internal
  * scratch fields filled with deterministic data.  Instrumentation for bench.py. */
 int tpmg_time_kernel(tpmg_hierarchy h, int kernel_id, int level, int reps, double* avg_ms);
+/* Kernel probes: with `enable` != 0, every later tpmg_pcg solve brackets its finest-level
+ * launches of TPMG_K_PCG_DIRECTION, _PCG_RUPDATE, _PCG_POSTSWEEP, _RESID_RESTRICT and
+ * _PROLONG_ADD with CUDA events on the library stream (recorded into the iteration's CUDA
+ * graph as external event nodes) and accumulates their device durations; enabling resets the
+ * totals.  tpmg_kernel_probe_read returns the total milliseconds and the launch count of one
+ * kernel id since then.  Instrumentation for bench.py (live durations inside the timed solves). */
+int tpmg_kernel_probe(tpmg_hierarchy h, int enable);
+int tpmg_kernel_probe_read(tpmg_hierarchy h, int kernel_id, double* total_ms, int64_t* launches);
 /* Enable/disable CUDA-graph replay of the PCG iteration (default on). */
 int tpmg_set_use_graphs(tpmg_hierarchy h, int enable);
 

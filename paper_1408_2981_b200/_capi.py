@@ -74,6 +74,8 @@ SIGNATURES = {
     "tpmg_kernel_launch_count": (C.c_int, [_VP, C.POINTER(C.c_int64)]),
     "tpmg_set_use_graphs": (C.c_int, [_VP, C.c_int]),
     "tpmg_time_kernel": (C.c_int, [_VP, C.c_int, C.c_int, C.c_int, _D]),
+    "tpmg_kernel_probe": (C.c_int, [_VP, C.c_int]),
+    "tpmg_kernel_probe_read": (C.c_int, [_VP, C.c_int, _D, C.POINTER(C.c_int64)]),
     "tpmg_profile_packed_size": (C.c_int64, [C.c_int, C.c_int64, C.c_int64, C.c_int64]),
     "tpmg_grid_fingerprint": (C.c_uint64, [_D, C.c_int64]),
     "tpmg_grid_fingerprint_cartesian": (C.c_uint64, [C.c_void_p]),

@@ -217,6 +217,19 @@ struct tpmg_hierarchy_s {
   tpmg::PcgLoop* h_loop = nullptr;  // pinned
   DevBuf d_hist;                    // |r| per iteration, kLoopHist entries
   static constexpr int kLoopHist = 4096;
+  // Kernel probes (tpmg_kernel_probe): a CUDA event pair around each probed finest-level PCG
+  // launch, recorded as external event nodes when the iteration is captured into its graph, read
+  // after every iteration's synchronisation: live per-launch durations inside a solve.
+  struct Probe {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    double total_ms = 0.0;
+    int64_t launches = 0;
+  };
+  static constexpr int kProbes = 16;
+  bool probe_on = false;
+  Probe probes[kProbes];
+  uint32_t probe_pending = 0;  // pairs recorded by the work queued since the last collection
+  std::unordered_map<const void*, uint32_t> iter_graph_probes;
   int finest() const { return (int)lv.size() - 1; }
   VertCoef vcoef() const {
     VertCoef v{d_bv.p, d_sv.p, d_av.p, d_xv.p};
@@ -240,6 +253,10 @@ struct tpmg_hierarchy_s {
     d_vx.upload(vx.data(), vx.size());
   }
   ~tpmg_hierarchy_s() {
+    for (auto& pr : probes) {
+      if (pr.e0) cudaEventDestroy(pr.e0);
+      if (pr.e1) cudaEventDestroy(pr.e1);
+    }
     for (auto& kv : iter_graphs) cudaGraphExecDestroy(kv.second);
     for (auto& kv : loop_graphs) cudaGraphExecDestroy(kv.second);
     if (d_loop) cudaFree(d_loop);
@@ -381,6 +398,33 @@ void finish_dot(tpmg_hierarchy h, int nblocks, int slot) {
                                 ctx->comm, ctx->stream));
 }
 
+// ---- kernel probes ----------------------------------------------------------------------
+void probe_begin(tpmg_hierarchy h, int id) {
+  if (!h->probe_on) return;
+  auto& pr = h->probes[id];
+  if (!pr.e0) {
+    CUDA_CHECK(cudaEventCreate(&pr.e0));
+    CUDA_CHECK(cudaEventCreate(&pr.e1));
+  }
+  CUDA_CHECK(cudaEventRecordWithFlags(pr.e0, h->ctx->stream, cudaEventRecordExternal));
+}
+void probe_end(tpmg_hierarchy h, int id) {
+  if (!h->probe_on) return;
+  CUDA_CHECK(cudaEventRecordWithFlags(h->probes[id].e1, h->ctx->stream, cudaEventRecordExternal));
+  h->probe_pending |= 1u << id;
+}
+// after a synchronisation: add the durations of the pairs recorded since the last one
+void probe_collect(tpmg_hierarchy h) {
+  for (int id = 0; id < tpmg_hierarchy_s::kProbes; ++id) {
+    if (!(h->probe_pending & (1u << id))) continue;
+    float ms = 0.f;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, h->probes[id].e0, h->probes[id].e1));
+    h->probes[id].total_ms += ms;
+    h->probes[id].launches += 1;
+  }
+  h->probe_pending = 0;
+}
+
 void dot_into(tpmg_hierarchy h, int64_t n, const double* a, const double* b, int slot) {
   int nb = 0;
   tpmg::launch_dot(h->ctx->launch(), n, a, b, h->partials.p, &nb);
@@ -401,14 +445,17 @@ void apply_level(tpmg_hierarchy h, int l, int mode, const double* u, const doubl
 // One line-Jacobi sweep.  With `fz` the sweep also does fused PCG work (see PcgFuse) and its
 // per-tile partials are reduced into scalar slot `slot`.
 void sweep(tpmg_hierarchy h, int l, const double* u_in, const double* f, double* out,
-           const tpmg::PcgFuse* fz = nullptr, int slot = -1, const tpmg::ProSrc* pro = nullptr) {
+           const tpmg::PcgFuse* fz = nullptr, int slot = -1, const tpmg::ProSrc* pro = nullptr,
+           int probe = -1) {
   Level& L = h->lv[l];
   // the haloed input: u, or p when the zero-guess sweep forms q = A p itself
   Halo H = u_in ? exchange(h, l, u_in)
                 : (fz && fz->p ? exchange(h, l, fz->p) : tpmg::self_halo(out, L.nx, L.ny, L.plane));
   int nb = 0;
+  if (probe >= 0) probe_begin(h, probe);
   tpmg::launch_jacobi(h->ctx->launch(), h->vcoef(), L.coef(h->nz), h->xi, u_in, H, f, out,
                       h->relax, h->d_err, fz, &nb, pro);
+  if (probe >= 0) probe_end(h, probe);
   if (fz) finish_dot(h, nb, slot);
 }
 
@@ -416,7 +463,7 @@ void sweep(tpmg_hierarchy h, int l, const double* u_in, const double* f, double*
 void restrict_plain(tpmg_hierarchy h, int lf, const double* fine, double* coarse);
 
 void resid_restrict(tpmg_hierarchy h, int lf, const double* u, const double* f, double* coarse,
-                    double* scratch) {
+                    double* scratch, bool probe = false) {
   Level& F = h->lv[lf];
   Level& C = h->lv[lf - 1];
   if (h->generic) {
@@ -429,8 +476,10 @@ void resid_restrict(tpmg_hierarchy h, int lf, const double* u, const double* f, 
     tpmg::launch_resid_restrict_sum(h->ctx->launch(), h->vcoef(), F.coef(h->nz), h->xi, u, H, f,
                                     coarse);
   } else if (!h->multi() && h->fuse_rr && tpmg::resid_restrict_T_fusable(F.coef(h->nz))) {
+    if (probe) probe_begin(h, TPMG_K_RESID_RESTRICT);
     tpmg::launch_resid_restrict_T(h->ctx->launch(), h->vcoef(), F.coef(h->nz), h->xi, u, f,
                                   coarse);
+    if (probe) probe_end(h, TPMG_K_RESID_RESTRICT);
   } else {
     apply_level(h, lf, tpmg::APPLY_RESID, u, f, scratch);
     const Halo Hr = exchange(h, lf, scratch);
@@ -454,7 +503,8 @@ void restrict_plain(tpmg_hierarchy h, int lf, const double* fine, double* coarse
   }
 }
 
-void prolong_level(tpmg_hierarchy h, int lc, const double* coarse, double* fine, bool add) {
+void prolong_level(tpmg_hierarchy h, int lc, const double* coarse, double* fine, bool add,
+                   bool probe = false) {
   Level& F = h->lv[lc + 1];
   const bool linear = h->prolongation == TPMG_PROLONG_LINEAR;
   if (h->generic) {
@@ -464,7 +514,9 @@ void prolong_level(tpmg_hierarchy h, int lc, const double* coarse, double* fine,
     return;
   }
   const Halo Hc = linear ? exchange(h, lc, coarse) : Halo{};
+  if (probe) probe_begin(h, TPMG_K_PROLONG_ADD);
   tpmg::launch_prolong(h->ctx->launch(), F.nx, F.ny, h->nz, coarse, Hc, fine, linear, add);
+  if (probe) probe_end(h, TPMG_K_PROLONG_ADD);
 }
 
 void fill(tpmg_hierarchy h, double* p, int64_t n, double v) {
@@ -501,7 +553,8 @@ void vcycle(tpmg_hierarchy h, int l, const double* f, double* A, double* B, bool
     if (npre > 0) {
       // first sweep from zero writes where the last sweep must end in A
       cur = ((total - 1) % 2 == 0) ? A : B;
-      sweep(h, l, nullptr, (pcg_fuse && f_pre) ? f_pre : f, cur, pcg_fuse ? &fz : nullptr, 2);
+      sweep(h, l, nullptr, (pcg_fuse && f_pre) ? f_pre : f, cur, pcg_fuse ? &fz : nullptr, 2,
+            nullptr, pcg_fuse ? TPMG_K_PCG_RUPDATE : -1);
       s0 = 1;
     } else {
       cur = (npost % 2 == 0) ? A : B;
@@ -518,7 +571,7 @@ void vcycle(tpmg_hierarchy h, int l, const double* f, double* A, double* B, bool
   bool fuse_pro = false;
   if (l > 0) {
     Level& C = h->lv[l - 1];
-    resid_restrict(h, l, cur, f, C.f.p, other(cur));
+    resid_restrict(h, l, cur, f, C.f.p, other(cur), pcg_fuse);
     vcycle(h, l - 1, C.f.p, C.u.p, C.t.p, true);
     fuse_pro = npost > 0 && !h->multi() && !h->generic &&
                h->prolongation == TPMG_PROLONG_LINEAR && tpmg::jacobi_prolong_fusable(L.coef(h->nz));
@@ -527,13 +580,14 @@ void vcycle(tpmg_hierarchy h, int l, const double* f, double* A, double* B, bool
       pro.cnx = (int)C.nx;
       pro.cny = (int)C.ny;
     } else {
-      prolong_level(h, l - 1, C.u.p, cur, true);
+      prolong_level(h, l - 1, C.u.p, cur, true, pcg_fuse);
     }
   }
   for (int s = 0; s < npost; ++s) {
     double* out = other(cur);
     const bool last = pcg_fuse && s + 1 == npost;
-    sweep(h, l, cur, f, out, last ? &fz : nullptr, 3, s == 0 && fuse_pro ? &pro : nullptr);
+    sweep(h, l, cur, f, out, last ? &fz : nullptr, 3, s == 0 && fuse_pro ? &pro : nullptr,
+          last ? TPMG_K_PCG_POSTSWEEP : -1);
     cur = out;
   }
   if (cur != A)
@@ -595,9 +649,11 @@ void pcg_iteration(tpmg_hierarchy h, double* x, bool first, int pc) {
       int nb = 0;
       // halos of z and p_old (single rank: the periodic self views, no copy)
       const Halo Hz = exchange(h, L, h->z.p, 0), Hp = exchange(h, L, po, 1);
+      probe_begin(h, TPMG_K_PCG_DIRECTION);
       tpmg::launch_pcg_ap(ctx->launch(), h->vcoef(), F.coef(h->nz), h->xi, h->z.p, Hz, po, Hp,
                           h->pbuf(pc ^ 1),
                           h->q_in_sweep ? nullptr : h->q.p, x, h->scal.p, h->partials.p, &nb);
+      probe_end(h, TPMG_K_PCG_DIRECTION);
       tpmg::launch_copy_scalar(ctx->launch(), h->scal.p, 0, 3);
       finish_dot(h, nb, 1);
       vcycle(h, L, h->r.p, h->z.p, h->tmp.p, true, true,
@@ -647,6 +703,8 @@ void run_iteration(tpmg_hierarchy h, double* x, bool first) {
     CUDA_CHECK(cudaStreamEndCapture(ctx->stream, &g));
     const int64_t nk = ctx->launches - before;
     ctx->launches = before;
+    h->iter_graph_probes[key] = h->probe_pending;  // recorded by every launch of this graph
+    h->probe_pending = 0;
     cudaGraphExec_t ge;
     CUDA_CHECK(cudaGraphInstantiate(&ge, g, 0));
     cudaGraphDestroy(g);
@@ -655,6 +713,7 @@ void run_iteration(tpmg_hierarchy h, double* x, bool first) {
   }
   CUDA_CHECK(cudaGraphLaunch(it->second, ctx->stream));
   ctx->launches += h->iter_graph_kernels[key];
+  h->probe_pending |= h->iter_graph_probes[key];
 }
 
 // Opt-in (TPMG_DEVLOOP=1, read per solve): bench.py measures the same solve time either way
@@ -1643,6 +1702,7 @@ int tpmg_pcg(tpmg_hierarchy h, tpmg_field f, tpmg_field x, double tol, int max_i
       run_iteration(h, x->buf.p, it == 1);
       CUDA_CHECK(cudaMemcpyAsync(h->h_scal, h->scal.p, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
       sync_check(h);
+      probe_collect(h);
       const double pq = h->h_scal[1], rr = h->h_scal[2], rho_new = h->h_scal[3];
       if (!(pq > 0.0)) {
         *solve_status = TPMG_BREAKDOWN;
@@ -1845,7 +1905,8 @@ int tpmg_time_kernel(tpmg_hierarchy h, int kernel_id, int level, int reps, doubl
     if (transfer && level < 1) throw Error(TPMG_E_SHAPE, "transfers need a fine level >= 1");
     Level& L = h->lv[level];
     const int64_t n = L.plane * h->nz;
-    const bool pcg_kernel = kernel_id == TPMG_K_PCG_DIRECTION || kernel_id == TPMG_K_PCG_RUPDATE;
+    const bool pcg_kernel = kernel_id == TPMG_K_PCG_DIRECTION || kernel_id == TPMG_K_PCG_RUPDATE ||
+                            kernel_id == TPMG_K_PCG_POSTSWEEP;
     if (pcg_kernel && !(tpmg::jacobi_fusable(h->lv[level].coef(h->nz)) &&
                         tpmg::pcg_ap_fusable(h->lv[level].coef(h->nz))))
       throw Error(TPMG_E_SHAPE, "the fused PCG kernels need a tiled level");
@@ -1894,6 +1955,14 @@ int tpmg_time_kernel(tpmg_hierarchy h, int kernel_id, int level, int reps, doubl
           sweep(h, level, nullptr, a.p, c.p, &fz, 2);
           break;
         }
+        case TPMG_K_PCG_POSTSWEEP: {  // u = a, r = b (the sweep's f), z = c; r.z partials
+          tpmg::PcgFuse fz;
+          fz.r = b.p;
+          fz.s = h->scal.p;
+          fz.partials = h->partials.p;
+          sweep(h, level, a.p, b.p, c.p, &fz, 3);
+          break;
+        }
         default: throw Error(TPMG_E_CONFIG, "unknown kernel id");
       }
     };
@@ -1911,6 +1980,35 @@ int tpmg_time_kernel(tpmg_hierarchy h, int kernel_id, int level, int reps, doubl
     cudaEventDestroy(e1);
     sync_check(h);
     *avg_ms = ms / reps;
+  });
+}
+
+int tpmg_kernel_probe(tpmg_hierarchy h, int enable) {
+  return guard(h->ctx, [&] {
+    if ((enable != 0) != h->probe_on) {  // cached iteration graphs carry (or lack) the probes
+      CUDA_CHECK(cudaStreamSynchronize(h->ctx->stream));
+      for (auto& kv : h->iter_graphs) cudaGraphExecDestroy(kv.second);
+      h->iter_graphs.clear();
+      h->iter_graph_kernels.clear();
+      h->iter_graph_probes.clear();
+      for (auto& kv : h->loop_graphs) cudaGraphExecDestroy(kv.second);
+      h->loop_graphs.clear();
+    }
+    h->probe_on = enable != 0;
+    h->probe_pending = 0;
+    for (auto& pr : h->probes) {
+      pr.total_ms = 0.0;
+      pr.launches = 0;
+    }
+  });
+}
+
+int tpmg_kernel_probe_read(tpmg_hierarchy h, int kernel_id, double* total_ms, int64_t* launches) {
+  return guard(h->ctx, [&] {
+    if (kernel_id < 0 || kernel_id >= tpmg_hierarchy_s::kProbes)
+      throw Error(TPMG_E_CONFIG, "unknown kernel id");
+    if (total_ms) *total_ms = h->probes[kernel_id].total_ms;
+    if (launches) *launches = h->probes[kernel_id].launches;
   });
 }
 

@@ -22,7 +22,7 @@ from ._capi import ContextParams, FactorizedProfiles, FullProfiles, GridDesc, MG
 
 K_FASTEST, X_FASTEST = 0, 1
 (K_APPLY, K_JACOBI, K_JACOBI_ZERO, K_RESID_RESTRICT, K_PROLONG_ADD, K_RESTRICT, K_RESIDUAL,
- K_PCG_DIRECTION, K_PCG_RUPDATE) = range(9)
+ K_PCG_DIRECTION, K_PCG_RUPDATE, K_PCG_POSTSWEEP) = range(10)
 LINEAR, INJECTION = 0, 1
 SUMMATION, TRANSPOSE = 0, 1
 OK, E_CONFIG, E_SHAPE, E_NONFINITE, E_FINGERPRINT, E_SINGULAR, E_CAP, E_CUDA, E_NCCL = range(9)
@@ -329,6 +329,17 @@ class Hierarchy:
                                                   self.finest if level is None else level, reps,
                                                   C.byref(out)))
         return out.value
+
+    def kernel_probe(self, on: bool = True):
+        """Live per-launch durations of the finest-level PCG kernels inside later pcg_solve
+        calls (CUDA events in the iteration graph); enabling resets the totals."""
+        self.ctx._check(self.lib.tpmg_kernel_probe(self._h, 1 if on else 0))
+
+    def kernel_probe_read(self, kernel_id: int):
+        """(total ms, launches) of one kernel id since kernel_probe(True)."""
+        ms, n = C.c_double(), C.c_int64()
+        self.ctx._check(self.lib.tpmg_kernel_probe_read(self._h, kernel_id, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
 
     def set_use_graphs(self, on: bool):
         self.lib.tpmg_set_use_graphs(self._h, 1 if on else 0)
