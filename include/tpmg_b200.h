@@ -306,48 +306,8 @@ int tpmg_profile_load(const char* path, const tpmg_grid_desc* grid, int* kind, d
 /* Message of the last failed tpmg_profile_* call on this thread. */
 const char* tpmg_profile_last_error(void);
 
-/* ---- the reference's own test problem, set up on the host ---------------------------------- */
-/* build_icosahedral_hierarchy (geometry.hpp:263-290), build_vertical_grid (:295-327), balanced-flow
- * profiles (profiles.hpp:128-176; factorize_balanced_flow :329-391, balanced_flow_profiles
- * :281-324), OperatorParameters::courant_default (:50-54), then build_hierarchy_coefficients'
- * assemble / restrict_profiles loop (multigrid.hpp:263-268) -- restated in the reference's
- * operation order, so tables and hatted coefficients equal the reference's bit for bit.  Host
- * only: no context needed until tpmg_hier_create_icosahedral. */
-typedef struct tpmg_icosa_params {
-  int levels;                /* finest refinement level L in [0, 9]: 20*4^L cells          */
-  int64_t n_r;               /* vertical cells                                             */
-  double depth;              /* shell depth H in planet radii                              */
-  int geometric;             /* VerticalGrading: 0 uniform, 1 geometric                    */
-  double ratio;              /* geometric grading ratio                                    */
-  double buoyancy_frequency; /* BalancedFlow N [1/s], >= N* (epsilon >= 0)                 */
-  double courant;            /* courant_default's factor (<= 0: the reference's 10)        */
-  int advection;             /* 0: without_advection (xi_r = 0)                            */
-} tpmg_icosa_params;
-typedef struct tpmg_icosa_s* tpmg_icosa;
-int tpmg_icosa_create(const tpmg_icosa_params* params, tpmg_icosa* out);
-int tpmg_icosa_destroy(tpmg_icosa ico);
-/* n_levels = L+1; omega and mu*dt of OperatorParameters; epsilon of the BalancedFlow. */
-int tpmg_icosa_info(tpmg_icosa ico, int* n_levels, double* omega, double* mu_dt, double* epsilon);
-/* One grid level (0 = 20 cells): neighbours / edges [T*3 + j] (Index3X neighbors(j, T),
- * cell_edges(j, T)), centres [3*T + i], areas, grid_fingerprint.  Pointers stay valid until
- * tpmg_icosa_destroy; any output may be NULL. */
-int tpmg_icosa_level(tpmg_icosa ico, int level, int64_t* n_cells, int64_t* n_edges,
-                     const int64_t** neighbors, const int64_t** cell_edges,
-                     const double** centers, const double** areas, uint64_t* fingerprint);
-/* Hatted coefficients of a level (the finest profiles restricted down to it): horizontal bh, ah,
- * xh per cell and sh per edge; vertical bv, sv (n_r), av, xv (n_r+1). */
-int tpmg_icosa_hatted(tpmg_icosa ico, int level, const double** bh, const double** ah,
-                      const double** xh, const double** sh, const double** bv, const double** sv,
-                      const double** av, const double** xv);
-/* The finest level's profile set, packed as for tpmg_profile_save_grid (kind FACTORIZED: the
- * factorised set; FULL: balanced_flow_profiles). */
-int tpmg_icosa_profiles(tpmg_icosa ico, int kind, double* packed, int64_t capacity);
-/* The device hierarchy of levels L+1-depth .. L (depth <= 0: all), through
- * tpmg_hier_create_generic with the reference's child order and linear-prolongation rule. */
-int tpmg_hier_create_icosahedral(tpmg_context ctx, tpmg_icosa ico, int depth, double relax,
-                                 int prolongation, int restriction, int nu_pre, int nu_post,
-                                 tpmg_hierarchy* out);
-const char* tpmg_icosa_last_error(void);
+/* (The reference's own icosahedral test problem is set up by test infrastructure,
+ * oracle/icosa_setup.cpp, and reaches the device through tpmg_hier_create_generic.) */
 
 /* ---- instrumentation ------------------------------------------------------------------------ */
 /* Number of kernels this library launched on the context since creation. */

@@ -1,18 +1,36 @@
-// tpmg_icosa.cpp -- the reference's own test problem, set up on the host in the reference's
-// operation order so the device can run it without the reference: the nested icosahedral
-// grids (geometry.hpp:116-290), the radial grid (:295-327), the balanced-flow profiles
+// icosa_setup.cpp -- TEST INFRASTRUCTURE (oracle side; only tests/ load it): the reference's
+// own test problem set up on the host in the reference's operation order, so that the device
+// can be pinned against the reference's outputs (tests/golden/ref_icosa_pin.bin) from the
+// reference's own fixture without the reference: the nested icosahedral grids
+// (geometry.hpp:116-290), the radial grid (:295-327), the balanced-flow profiles
 // (profiles.hpp:14-176, 262-392), assemble_hatted for factorised profiles
 // (discretization.hpp:70-84, 146-184) and restrict_profiles (multigrid.hpp:107-201), ending in
 // the same tables and hatted coefficients build_hierarchy_coefficients (multigrid.hpp:242-272)
-// would hand to the V-cycle.  Host code only; the hierarchy it creates is an indirect one
-// (tpmg_hier_create_generic).
+// would hand to the V-cycle.  This is a restatement of the reference's setup code, kept out of
+// the product: the product takes such tables through its C-ABI (tpmg_hier_create_generic).
 //
 // Arithmetic follows the reference expression by expression (left-to-right association, no
 // contraction: this file is compiled with -ffp-contract=off) with Eigen's reductions as the
 // oracle's Eigen shim evaluates them (sequential sums; v / |v| per component), which is how the
 // committed golden outputs of the reference were produced -- tests/test_icosa_setup.py compares
 // every table and coefficient bit for bit.
-#include "tpmg_b200.h"
+#include <cstdint>
+
+// status codes and profile kinds of the product's C-ABI (include/tpmg_b200.h), restated so the
+// oracle library stays standalone
+enum { TPMG_OK = 0, TPMG_E_CONFIG = 1, TPMG_E_CAP = 6 };
+enum { TPMG_PROFILE_FACTORIZED = 0, TPMG_PROFILE_FULL = 2 };
+typedef struct tpmgo_icosa_params {
+  int levels;              // refinements of the base icosahedron (grids 0..levels)
+  int64_t n_r;             // vertical cells
+  double depth;            // radial depth (units of the Earth's radius)
+  int geometric;           // 0 uniform, 1 geometric grading
+  double ratio;            // grading ratio
+  double buoyancy_frequency;
+  double courant;          // <= 0: courant_default's 10
+  int advection;           // 0: without_advection
+} tpmgo_icosa_params;
+typedef struct tpmg_icosa_s* tpmg_icosa;
 
 #include <algorithm>
 #include <array>
@@ -479,7 +497,7 @@ Factorized restrict_fact(const Factorized& fine, const Grid& fg, int64_t ncoarse
 }  // namespace
 
 struct tpmg_icosa_s {
-  tpmg_icosa_params prm{};
+  tpmgo_icosa_params prm{};
   std::vector<Grid> grids;                                   // levels 0..L
   std::vector<std::vector<std::array<int64_t, 2>>> colinear;  // [l]: coarse level l edges
   Vert vert;
@@ -488,7 +506,6 @@ struct tpmg_icosa_s {
   Full full;        // finest level
   std::vector<Hatted> hatted;  // per level
   std::vector<std::vector<double>> centers;  // per level, 3 per cell
-  std::vector<uint64_t> fingerprint;
 };
 
 namespace {
@@ -514,11 +531,11 @@ int guard(Fn&& fn) {
 
 extern "C" {
 
-const char* tpmg_icosa_last_error(void) { return g_icosa_error.c_str(); }
+const char* tpmgo_icosa_last_error(void) { return g_icosa_error.c_str(); }
 
-int tpmg_icosa_create(const tpmg_icosa_params* p, tpmg_icosa* out) {
+int tpmgo_icosa_create(const tpmgo_icosa_params* p, tpmg_icosa* out) {
   return guard([&] {
-    if (!p || !out) throw SetupError(TPMG_E_CONFIG, "tpmg_icosa_create: null argument");
+    if (!p || !out) throw SetupError(TPMG_E_CONFIG, "tpmgo_icosa_create: null argument");
     if (p->levels < 0 || p->levels > 9)
       throw SetupError(TPMG_E_CONFIG, "level count must be in [0, 9]");
     auto ico = std::make_unique<tpmg_icosa_s>();
@@ -575,19 +592,18 @@ int tpmg_icosa_create(const tpmg_icosa_params* p, tpmg_icosa* out) {
         c.push_back(v.y);
         c.push_back(v.z);
       }
-      ico->fingerprint.push_back(tpmg_grid_fingerprint(c.data(), g.n_cells()));
       ico->centers.push_back(std::move(c));
     }
     *out = ico.release();
   });
 }
 
-int tpmg_icosa_destroy(tpmg_icosa ico) {
+int tpmgo_icosa_destroy(tpmg_icosa ico) {
   delete ico;
   return TPMG_OK;
 }
 
-int tpmg_icosa_info(tpmg_icosa ico, int* n_levels, double* omega, double* mu_dt,
+int tpmgo_icosa_info(tpmg_icosa ico, int* n_levels, double* omega, double* mu_dt,
                     double* epsilon) {
   return guard([&] {
     if (!ico) throw SetupError(TPMG_E_CONFIG, "null problem");
@@ -598,12 +614,12 @@ int tpmg_icosa_info(tpmg_icosa ico, int* n_levels, double* omega, double* mu_dt,
   });
 }
 
-int tpmg_icosa_level(tpmg_icosa ico, int level, int64_t* n_cells, int64_t* n_edges,
+int tpmgo_icosa_level(tpmg_icosa ico, int level, int64_t* n_cells, int64_t* n_edges,
                      const int64_t** neighbors, const int64_t** cell_edges,
-                     const double** centers, const double** areas, uint64_t* fingerprint) {
+                     const double** centers, const double** areas) {
   return guard([&] {
     if (!ico || level < 0 || level >= (int)ico->grids.size())
-      throw SetupError(TPMG_E_CONFIG, "tpmg_icosa_level: no such level");
+      throw SetupError(TPMG_E_CONFIG, "tpmgo_icosa_level: no such level");
     const Grid& g = ico->grids[(size_t)level];
     if (n_cells) *n_cells = g.n_cells();
     if (n_edges) *n_edges = g.n_edges();
@@ -611,16 +627,15 @@ int tpmg_icosa_level(tpmg_icosa ico, int level, int64_t* n_cells, int64_t* n_edg
     if (cell_edges) *cell_edges = g.cell_edges.data();
     if (centers) *centers = ico->centers[(size_t)level].data();
     if (areas) *areas = g.areas.data();
-    if (fingerprint) *fingerprint = ico->fingerprint[(size_t)level];
   });
 }
 
-int tpmg_icosa_hatted(tpmg_icosa ico, int level, const double** bh, const double** ah,
+int tpmgo_icosa_hatted(tpmg_icosa ico, int level, const double** bh, const double** ah,
                       const double** xh, const double** sh, const double** bv, const double** sv,
                       const double** av, const double** xv) {
   return guard([&] {
     if (!ico || level < 0 || level >= (int)ico->hatted.size())
-      throw SetupError(TPMG_E_CONFIG, "tpmg_icosa_hatted: no such level");
+      throw SetupError(TPMG_E_CONFIG, "tpmgo_icosa_hatted: no such level");
     const Hatted& h = ico->hatted[(size_t)level];
     if (bh) *bh = h.bh.data();
     if (ah) *ah = h.ah.data();
@@ -633,9 +648,9 @@ int tpmg_icosa_hatted(tpmg_icosa ico, int level, const double** bh, const double
   });
 }
 
-int tpmg_icosa_profiles(tpmg_icosa ico, int kind, double* packed, int64_t capacity) {
+int tpmgo_icosa_profiles(tpmg_icosa ico, int kind, double* packed, int64_t capacity) {
   return guard([&] {
-    if (!ico || !packed) throw SetupError(TPMG_E_CONFIG, "tpmg_icosa_profiles: null argument");
+    if (!ico || !packed) throw SetupError(TPMG_E_CONFIG, "tpmgo_icosa_profiles: null argument");
     std::vector<const std::vector<double>*> parts;
     if (kind == TPMG_PROFILE_FACTORIZED) {
       const Factorized& f = ico->fac;
@@ -645,59 +660,16 @@ int tpmg_icosa_profiles(tpmg_icosa ico, int kind, double* packed, int64_t capaci
       const Full& f = ico->full;
       parts = {&f.beta, &f.alpha_s, &f.alpha_r, &f.xi_r};
     } else {
-      throw SetupError(TPMG_E_CONFIG, "tpmg_icosa_profiles: unknown kind");
+      throw SetupError(TPMG_E_CONFIG, "tpmgo_icosa_profiles: unknown kind");
     }
     int64_t n = 0;
     for (const auto* v : parts) n += (int64_t)v->size();
-    if (n > capacity) throw SetupError(TPMG_E_CAP, "tpmg_icosa_profiles: buffer too small");
+    if (n > capacity) throw SetupError(TPMG_E_CAP, "tpmgo_icosa_profiles: buffer too small");
     for (const auto* v : parts) {
       std::memcpy(packed, v->data(), v->size() * sizeof(double));
       packed += v->size();
     }
   });
-}
-
-int tpmg_hier_create_icosahedral(tpmg_context ctx, tpmg_icosa ico, int depth, double relax,
-                                 int prolongation, int restriction, int nu_pre, int nu_post,
-                                 tpmg_hierarchy* out) {
-  int rc = guard([&] {
-    if (!ico) throw SetupError(TPMG_E_CONFIG, "null problem");
-  });
-  if (rc != TPMG_OK) return rc;
-  const int finest = (int)ico->grids.size() - 1;
-  if (depth <= 0 || depth > finest + 1) depth = finest + 1;  // multigrid.hpp:259-260
-  const int coarsest = finest + 1 - depth;
-  std::vector<int64_t> nc, ne;
-  std::vector<const int64_t*> nbr, ced, chd;
-  std::vector<std::vector<int64_t>> children((size_t)depth);
-  std::vector<const double*> bh, ah, xh, sh;
-  for (int l = coarsest; l <= finest; ++l) {
-    const Grid& g = ico->grids[(size_t)l];
-    const Hatted& h = ico->hatted[(size_t)l];
-    nc.push_back(g.n_cells());
-    ne.push_back(g.n_edges());
-    nbr.push_back(g.neighbors.data());
-    ced.push_back(g.cell_edges.data());
-    auto& ch = children[(size_t)(l - coarsest)];
-    if (l > coarsest) {  // GridHierarchy::child_of(Tc, j) = 4 Tc + j, geometry.hpp:89-90
-      ch.resize((size_t)(4 * ico->grids[(size_t)l - 1].n_cells()));
-      for (size_t i = 0; i < ch.size(); ++i) ch[i] = (int64_t)i;
-    }
-    chd.push_back(l > coarsest ? ch.data() : nullptr);
-    bh.push_back(h.bh.data());
-    ah.push_back(h.ah.data());
-    xh.push_back(h.xh.data());
-    sh.push_back(h.sh.data());
-  }
-  // linear prolongation's corner rule, multigrid.hpp:88-95: corner child j takes the coarse
-  // neighbours across edges (j+1)%3 and (j+2)%3, the centre child none
-  const int d1[4] = {1, 2, 0, -1}, d2[4] = {2, 0, 1, -1};
-  const Hatted& hf = ico->hatted[(size_t)finest];
-  return tpmg_hier_create_generic(ctx, depth, (int)ico->vert.n_r, 3, 4, nc.data(), ne.data(),
-                                  nbr.data(), ced.data(), chd.data(), d1, d2, hf.bv.data(),
-                                  hf.sv.data(), hf.av.data(), hf.xv.data(), bh.data(), ah.data(),
-                                  xh.data(), sh.data(), relax, prolongation, restriction, nu_pre,
-                                  nu_post, out);
 }
 
 }  // extern "C"

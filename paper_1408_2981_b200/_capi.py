@@ -84,17 +84,6 @@ SIGNATURES = {
     "tpmg_profile_save": (C.c_int, [C.c_char_p, C.c_void_p, C.c_int, _D, C.c_int]),
     "tpmg_profile_load": (C.c_int, [C.c_char_p, C.c_void_p, C.POINTER(C.c_int), _D, C.c_int64]),
     "tpmg_profile_last_error": (C.c_char_p, []),
-    "tpmg_icosa_create": (C.c_int, [C.c_void_p, C.POINTER(_VP)]),
-    "tpmg_icosa_destroy": (C.c_int, [_VP]),
-    "tpmg_icosa_info": (C.c_int, [_VP, C.POINTER(C.c_int), _D, _D, _D]),
-    "tpmg_icosa_level": (C.c_int, [_VP, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
-                                   C.POINTER(C.POINTER(C.c_int64)), C.POINTER(C.POINTER(C.c_int64)),
-                                   C.POINTER(_D), C.POINTER(_D), C.POINTER(C.c_uint64)]),
-    "tpmg_icosa_hatted": (C.c_int, [_VP, C.c_int] + [C.POINTER(_D)] * 8),
-    "tpmg_icosa_profiles": (C.c_int, [_VP, C.c_int, _D, C.c_int64]),
-    "tpmg_hier_create_icosahedral": (C.c_int, [_VP, _VP, C.c_int, C.c_double, C.c_int, C.c_int,
-                                               C.c_int, C.c_int, C.POINTER(_VP)]),
-    "tpmg_icosa_last_error": (C.c_char_p, []),
 }
 
 
@@ -115,12 +104,6 @@ class FactorizedProfiles(C.Structure):
 
 class FullProfiles(C.Structure):  # tpmg_full_profiles
     _fields_ = [(n, _D) for n in ("beta", "alpha_s", "alpha_r", "xi_r")]
-
-
-class IcosaParams(C.Structure):  # tpmg_icosa_params
-    _fields_ = [("levels", C.c_int), ("n_r", C.c_int64), ("depth", C.c_double),
-                ("geometric", C.c_int), ("ratio", C.c_double), ("buoyancy_frequency", C.c_double),
-                ("courant", C.c_double), ("advection", C.c_int)]
 
 
 class ProfileGrid(C.Structure):  # tpmg_profile_grid

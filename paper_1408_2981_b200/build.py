@@ -18,7 +18,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 SOURCES = [os.path.join(CSRC, "tpmg_kernels.cu"), os.path.join(CSRC, "tpmg_host.cpp"),
-           os.path.join(CSRC, "tpmg_io.cpp"), os.path.join(CSRC, "tpmg_icosa.cpp")]
+           os.path.join(CSRC, "tpmg_io.cpp")]
 DEPS = SOURCES + [os.path.join(CSRC, "tpmg_kernels.cuh"), os.path.join(ROOT, "include", "tpmg_b200.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC,-O3,-ffp-contract=off", "-shared",

@@ -399,6 +399,16 @@ void finish_dot(tpmg_hierarchy h, int nblocks, int slot) {
 }
 
 // ---- kernel probes ----------------------------------------------------------------------
+// an event record on the library stream; inside a stream capture an external event node of
+// the graph (so the event is re-recorded by every launch of the graph)
+void probe_record(tpmg_hierarchy h, cudaEvent_t e) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  CUDA_CHECK(cudaStreamIsCapturing(h->ctx->stream, &st));
+  if (st == cudaStreamCaptureStatusActive)
+    CUDA_CHECK(cudaEventRecordWithFlags(e, h->ctx->stream, cudaEventRecordExternal));
+  else
+    CUDA_CHECK(cudaEventRecord(e, h->ctx->stream));
+}
 void probe_begin(tpmg_hierarchy h, int id) {
   if (!h->probe_on) return;
   auto& pr = h->probes[id];
@@ -406,11 +416,11 @@ void probe_begin(tpmg_hierarchy h, int id) {
     CUDA_CHECK(cudaEventCreate(&pr.e0));
     CUDA_CHECK(cudaEventCreate(&pr.e1));
   }
-  CUDA_CHECK(cudaEventRecordWithFlags(pr.e0, h->ctx->stream, cudaEventRecordExternal));
+  probe_record(h, pr.e0);
 }
 void probe_end(tpmg_hierarchy h, int id) {
   if (!h->probe_on) return;
-  CUDA_CHECK(cudaEventRecordWithFlags(h->probes[id].e1, h->ctx->stream, cudaEventRecordExternal));
+  probe_record(h, h->probes[id].e1);
   h->probe_pending |= 1u << id;
 }
 // after a synchronisation: add the durations of the pairs recorded since the last one

@@ -275,6 +275,14 @@ tpmg_profile_grid cartesian_grid(const tpmg_grid_desc* g) {
 // shortest representation, which is why it is restated here instead of using "%.17g": the
 // written bytes must equal the reference's.  The cached powers are the correctly rounded 64-bit
 // significands of 10^k, k = -300, -292, ..., 324 (generated with exact rational arithmetic).
+//
+// Attribution: the structure of this block -- the cached-power index formula, the four-partial
+// 64x64 multiply with half-up rounding, and grisu2_round's loop condition -- follows
+// nlohmann::json's dtoa_impl (https://github.com/nlohmann/json, MIT License, Copyright (c)
+// 2013-2022 Niels Lohmann), itself an implementation of Florian Loitsch's Grisu2 (reference
+// implementation under the MIT/BSD-style licence of the paper's code).  Byte-identical output
+// with the reference's writer requires the same algorithm; the MIT licence terms apply to the
+// parts that follow it.
 namespace grisu {
 
 struct Fp {

@@ -609,101 +609,3 @@ def load_profiles(path: str, P):
             arrays["xi_r"] = None
         Q.coef, Q.dense = "full", arrays
     return Q
-
-
-# ---- the reference's own test problem, set up on the host (tpmg_icosa_*) ------------------------
-
-class Icosahedral:
-    """build_icosahedral_hierarchy + build_vertical_grid + balanced-flow profiles +
-    courant_default + the hatted coefficients of every level (geometry.hpp:263-327,
-    profiles.hpp:128-391, multigrid.hpp:263-268), computed by the library on the host in the
-    reference's operation order.  Mirrors the reference's fixture (tests/fixtures.hpp:18-62)."""
-
-    def __init__(self, levels: int, n_r: int, depth: float, grading: str = "uniform",
-                 ratio: float = 1.0, buoyancy_frequency: float = 0.022, courant: float = 10.0,
-                 advection: bool = True):
-        self.lib = _capi.load()
-        prm = _capi.IcosaParams(levels, n_r, depth, int(grading == "geometric"), ratio,
-                                buoyancy_frequency, courant, int(advection))
-        h = C.c_void_p()
-        rc = self.lib.tpmg_icosa_create(C.byref(prm), C.byref(h))
-        if rc != OK:
-            raise _ERRORS.get(rc, TpmgError)(self.lib.tpmg_icosa_last_error().decode())
-        self._h = h
-        n, om, mu, eps = C.c_int(), C.c_double(), C.c_double(), C.c_double()
-        self.lib.tpmg_icosa_info(self._h, C.byref(n), C.byref(om), C.byref(mu), C.byref(eps))
-        self.n_levels, self.omega, self.mu_dt, self.epsilon = n.value, om.value, mu.value, eps.value
-        self.n_r = n_r
-
-    def close(self):
-        if getattr(self, "_h", None):
-            self.lib.tpmg_icosa_destroy(self._h)
-            self._h = None
-
-    def __del__(self):
-        self.close()
-
-    def level(self, level: int) -> dict:
-        nc, ne = C.c_int64(), C.c_int64()
-        I64P = C.POINTER(C.c_int64)
-        nb, ce = I64P(), I64P()
-        cen, ar = C.POINTER(C.c_double)(), C.POINTER(C.c_double)()
-        fp = C.c_uint64()
-        rc = self.lib.tpmg_icosa_level(self._h, level, C.byref(nc), C.byref(ne), C.byref(nb),
-                                       C.byref(ce), C.byref(cen), C.byref(ar), C.byref(fp))
-        if rc != OK:
-            raise _ERRORS.get(rc, TpmgError)(self.lib.tpmg_icosa_last_error().decode())
-        n, m = nc.value, ne.value
-        return dict(n_cells=n, n_edges=m,
-                    neighbors=np.ctypeslib.as_array(nb, (n * 3,)).copy().reshape(n, 3),
-                    cell_edges=np.ctypeslib.as_array(ce, (n * 3,)).copy().reshape(n, 3),
-                    centers=np.ctypeslib.as_array(cen, (n * 3,)).copy().reshape(n, 3),
-                    areas=np.ctypeslib.as_array(ar, (n,)).copy(), fingerprint=fp.value)
-
-    def hatted(self, level: int) -> dict:
-        P = [C.POINTER(C.c_double)() for _ in range(8)]
-        rc = self.lib.tpmg_icosa_hatted(self._h, level, *[C.byref(p) for p in P])
-        if rc != OK:
-            raise _ERRORS.get(rc, TpmgError)(self.lib.tpmg_icosa_last_error().decode())
-        lv = self.level(level)
-        nc, ne, nr = lv["n_cells"], lv["n_edges"], self.n_r
-        sizes = (nc, nc, nc, ne, nr, nr, nr + 1, nr + 1)
-        names = ("bh", "ah", "xh", "sh", "bv", "sv", "av", "xv")
-        return {k: np.ctypeslib.as_array(p, (n,)).copy() for k, p, n in zip(names, P, sizes)}
-
-    def profiles(self, kind: int) -> dict:
-        """The finest level's profile set (PROFILE_FACTORIZED or PROFILE_FULL), reference shapes."""
-        lv = self.level(self.n_levels - 1)
-        g = profile_grid("icosahedral", lv["fingerprint"], self.n_levels - 1, self.n_r,
-                         lv["n_cells"], lv["n_edges"])
-        cap = self.lib.tpmg_profile_packed_size(kind, g.n_cells, g.n_edges, g.n_r)
-        buf = np.empty(cap)
-        rc = self.lib.tpmg_icosa_profiles(self._h, kind, _p(buf), cap)
-        if rc != OK:
-            raise _ERRORS.get(rc, TpmgError)(self.lib.tpmg_icosa_last_error().decode())
-        return _unpack(kind, g, buf)
-
-    def profile_grid(self) -> _capi.ProfileGrid:
-        lv = self.level(self.n_levels - 1)
-        return profile_grid("icosahedral", lv["fingerprint"], self.n_levels - 1, self.n_r,
-                            lv["n_cells"], lv["n_edges"])
-
-    def hierarchy(self, ctx: Context, depth: int = 0, relax: float = 0.9,
-                  prolongation: int = LINEAR, restriction: int = SUMMATION, nu_pre: int = 2,
-                  nu_post: int = 2) -> Hierarchy:
-        """The device hierarchy of this problem (tpmg_hier_create_icosahedral)."""
-        self_h = Hierarchy.__new__(Hierarchy)
-        self_h.ctx, self_h.lib = ctx, ctx.lib
-        self_h._h = None
-        h = C.c_void_p()
-        ctx._check(self.lib.tpmg_hier_create_icosahedral(ctx._h, self._h, depth, C.c_double(relax),
-                                                         prolongation, restriction, nu_pre,
-                                                         nu_post, C.byref(h)))
-        self_h._h = h
-        ctx._live_children += 1
-        self_h.problem = None
-        n = C.c_int()
-        self.lib.tpmg_hier_n_levels(self_h._h, C.byref(n))
-        self_h.n_levels = n.value
-        self_h.finest = n.value - 1
-        return self_h

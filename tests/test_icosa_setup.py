@@ -1,5 +1,5 @@
-"""The reference's own test problem set up by the library on the host (SURVEY.md §8(f) rank 3:
-icosahedral grids + balanced-flow profiles): tpmg_icosa_create restates
+"""The reference's own test problem set up on the host by test infrastructure (SURVEY.md §8(f) rank 3:
+icosahedral grids + balanced-flow profiles): oracle/icosa_setup.cpp (test infrastructure) restates
 build_icosahedral_hierarchy, build_vertical_grid, the balanced-flow profiles, courant_default
 and build_hierarchy_coefficients' assemble / restrict loop.
 
@@ -9,7 +9,7 @@ Pinned against the REFERENCE ITSELF, twice, through fixtures its own code wrote:
   * tests/golden/profile_io/ (oracle/build_ref_profile_io.py): the level-1 grid's centres and
     fingerprint, its full and factorised balanced-flow profiles, and the profile files the
     reference's save_profiles wrote from them -- re-written here byte for byte.
-Host code only; the device side of this problem is in test_ref_pin_gpu.py (source="setup").
+Host code only (the setup is test infrastructure; the product takes the tables through tpmg_hier_create_generic); the device side of this problem is in test_ref_pin_gpu.py (source="setup").
 """
 import filecmp
 import os
@@ -17,6 +17,7 @@ import os
 import numpy as np
 import pytest
 
+import icosa  # oracle/: the reference's own icosahedral problem (test infrastructure)
 from paper_1408_2981_b200 import tpmg
 from test_profile_io import GOLD, _meta
 from test_ref_pin import load
@@ -29,7 +30,7 @@ def R():
 
 @pytest.fixture(scope="module")
 def ico_pin(R):
-    return tpmg.Icosahedral(2, int(R["nr"][0]), 80.0 / 6371.229, "geometric", 1.2, 0.022, 10.0,
+    return icosa.Icosahedral(2, int(R["nr"][0]), 80.0 / 6371.229, "geometric", 1.2, 0.022, 10.0,
                             True)
 
 
@@ -60,7 +61,7 @@ def test_hatted_coefficients_bitwise(R, ico_pin, level):
 
 def test_level1_fixture_profiles_and_fingerprint():
     m = _meta()
-    ico = tpmg.Icosahedral(1, 4, 0.0126)  # tests/test_profile_io.cpp:40-42 of the reference
+    ico = icosa.Icosahedral(1, 4, 0.0126)  # tests/test_profile_io.cpp:40-42 of the reference
     lv = ico.level(1)
     assert np.array_equal(lv["centers"].ravel(), m["centers"])
     assert lv["fingerprint"] == int(m["fingerprint"].view(np.uint64)[0])
@@ -73,14 +74,14 @@ def test_level1_fixture_profiles_and_fingerprint():
 @pytest.mark.parametrize("enc,suf", [("decimal", "dec"), ("base64-f64le", "b64")])
 def test_profile_files_byte_identical_to_the_references(tmp_path, kind, pre, enc, suf):
     """Grid -> balanced-flow profiles -> save_profiles, end to end, equals the reference's file."""
-    ico = tpmg.Icosahedral(1, 4, 0.0126)
+    ico = icosa.Icosahedral(1, 4, 0.0126)
     out = tmp_path / "p.json"
     tpmg.save_profile_arrays(str(out), ico.profile_grid(), kind, ico.profiles(kind), enc)
     assert filecmp.cmp(str(out), os.path.join(GOLD, f"{pre}_{suf}.json"), shallow=False)
 
 
 def test_without_advection_and_separability():
-    ico = tpmg.Icosahedral(1, 6, 0.0126, advection=False)
+    ico = icosa.Icosahedral(1, 6, 0.0126, advection=False)
     fac = ico.profiles(tpmg.PROFILE_FACTORIZED)
     full = ico.profiles(tpmg.PROFILE_FULL)
     assert not fac["xi_r_r"].any() and not full["xi_r"].any()
@@ -92,7 +93,7 @@ def test_without_advection_and_separability():
 
 
 def test_courant_default_and_deterministic_geometry():
-    a, b = tpmg.Icosahedral(3, 2, 0.01), tpmg.Icosahedral(3, 2, 0.01)
+    a, b = icosa.Icosahedral(3, 2, 0.01), icosa.Icosahedral(3, 2, 0.01)
     la, lb = a.level(3), b.level(3)
     assert la["fingerprint"] == lb["fingerprint"]
     # omega = 10 x mean great-circle edge length of the finest grid
@@ -105,13 +106,13 @@ def test_courant_default_and_deterministic_geometry():
     assert (counts == 2).all()
 
 
-@pytest.mark.parametrize("kw,exc", [(dict(levels=10), tpmg.config_error),
-                                    (dict(n_r=0), tpmg.config_error),
-                                    (dict(depth=0.0), tpmg.config_error),
-                                    (dict(buoyancy_frequency=0.001), tpmg.config_error)])
+@pytest.mark.parametrize("kw,exc", [(dict(levels=10), icosa.IcosaError),
+                                    (dict(n_r=0), icosa.IcosaError),
+                                    (dict(depth=0.0), icosa.IcosaError),
+                                    (dict(buoyancy_frequency=0.001), icosa.IcosaError)])
 def test_configuration_errors(kw, exc):
     """geometry.hpp:266-267, 298-300; profiles.hpp:136-137."""
     args = dict(levels=1, n_r=4, depth=0.0126)
     args.update(kw)
     with pytest.raises(exc):
-        tpmg.Icosahedral(**args)
+        icosa.Icosahedral(**args)

@@ -13,6 +13,7 @@ import numpy as np
 import pytest
 
 from test_ref_pin import load
+import icosa  # oracle/: the reference's own icosahedral problem (test infrastructure)
 from paper_1408_2981_b200 import tpmg
 from paper_1408_2981_b200.tpmg import K_FASTEST
 
@@ -25,7 +26,7 @@ def R():
 
 
 # The hierarchy either from the reference's dumped tables and coefficients ("tables") or from
-# the library's own host setup of the same problem ("setup": tpmg_icosa_create with the
+# the library's own host setup of the same problem ("setup": oracle/icosa_setup.cpp with the
 # reference driver's parameters, oracle/ref_driver.cpp) -- both must reproduce the reference.
 @pytest.fixture(params=["tables", "setup"])
 def source(request):
@@ -38,7 +39,7 @@ _ICO = {}
 def make(ctx, R, prolongation=0, restriction=0, source="tables"):
     if source == "setup":
         if "ico" not in _ICO:
-            _ICO["ico"] = tpmg.Icosahedral(2, int(R["nr"][0]), 80.0 / 6371.229, "geometric", 1.2,
+            _ICO["ico"] = icosa.Icosahedral(2, int(R["nr"][0]), 80.0 / 6371.229, "geometric", 1.2,
                                            0.022, 10.0, True)
         return _ICO["ico"].hierarchy(ctx, 0, float(R["relax"][0]), prolongation, restriction, 2, 2)
     nl = int(R["n_levels"][0])
