@@ -323,7 +323,8 @@ typedef enum tpmg_kernel_id {
   TPMG_K_RESIDUAL = 6,        /* r = f - A u                              */
   TPMG_K_PCG_DIRECTION = 7,   /* fused PCG pass: x += a p; p = z + b p; A p and p.(A p) */
   TPMG_K_PCG_RUPDATE = 8,     /* fused PCG pre-sweep: r -= a A p, |r|^2, z = smoother(r) */
-  TPMG_K_PCG_POSTSWEEP = 9    /* fused PCG post-sweep: z = smoother(u) and the r.z partials */
+  TPMG_K_PCG_POSTSWEEP = 9,   /* fused PCG post-sweep: z = smoother(u) and the r.z partials */
+  TPMG_K_REDUCE = 10          /* (probe only) fixed-order final sum of a dot's partials   */
 } tpmg_kernel_id;
 /* Average device time (CUDA events on the library's stream) of `reps` back-to-back launches
  * of one hot-path kernel on `level` (transfers: `level` is the fine level), on internal

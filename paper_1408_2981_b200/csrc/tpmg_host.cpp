@@ -12,6 +12,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -390,9 +391,13 @@ Halo exchange(tpmg_hierarchy h, int l, const double* u, int set = 0) {
 }
 
 // s[slot] = global sum of the per-block partials.
+void probe_begin(tpmg_hierarchy h, int id);
+void probe_end(tpmg_hierarchy h, int id);
 void finish_dot(tpmg_hierarchy h, int nblocks, int slot) {
   tpmg_context ctx = h->ctx;
+  probe_begin(h, TPMG_K_REDUCE);
   tpmg::launch_reduce(ctx->launch(), h->partials.p, nblocks, h->scal.p + slot);
+  probe_end(h, TPMG_K_REDUCE);
   if (ctx->world > 1)
     NCCL_CHECK(g_nccl.AllReduce(h->scal.p + slot, h->scal.p + slot, 1, ncclDouble, ncclSum,
                                 ctx->comm, ctx->stream));
@@ -1682,6 +1687,10 @@ int tpmg_pcg(tpmg_hierarchy h, tpmg_field f, tpmg_field x, double tol, int max_i
         sync_check(h);
       }
     };
+    static const bool debug_timing = [] {
+      const char* e = getenv("TPMG_DEBUG_TIMING");
+      return e && atoi(e) != 0;
+    }();
     for (int it = 1; it <= max_iter; ++it) {
       if (it == 2 && device_loop_ok(h, max_iter)) {
         // iterations 2.. as one graph launch: the convergence test runs on the device
@@ -1709,10 +1718,18 @@ int tpmg_pcg(tpmg_hierarchy h, tpmg_field f, tpmg_field x, double tol, int max_i
           default: *solve_status = TPMG_NOT_CONVERGED; finish_x(); return;
         }
       }
+      const auto t_a = std::chrono::steady_clock::now();
       run_iteration(h, x->buf.p, it == 1);
+      const auto t_b = std::chrono::steady_clock::now();
       CUDA_CHECK(cudaMemcpyAsync(h->h_scal, h->scal.p, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
       sync_check(h);
       probe_collect(h);
+      if (debug_timing) {  // TPMG_DEBUG_TIMING=1: host time to queue / wait for each iteration
+        const auto t_c = std::chrono::steady_clock::now();
+        fprintf(stderr, "[tpmg] it %d queue %.1f us wait %.1f us\n", it,
+                std::chrono::duration<double, std::micro>(t_b - t_a).count(),
+                std::chrono::duration<double, std::micro>(t_c - t_b).count());
+      }
       const double pq = h->h_scal[1], rr = h->h_scal[2], rho_new = h->h_scal[3];
       if (!(pq > 0.0)) {
         *solve_status = TPMG_BREAKDOWN;

@@ -22,7 +22,7 @@ from ._capi import ContextParams, FactorizedProfiles, FullProfiles, GridDesc, MG
 
 K_FASTEST, X_FASTEST = 0, 1
 (K_APPLY, K_JACOBI, K_JACOBI_ZERO, K_RESID_RESTRICT, K_PROLONG_ADD, K_RESTRICT, K_RESIDUAL,
- K_PCG_DIRECTION, K_PCG_RUPDATE, K_PCG_POSTSWEEP) = range(10)
+ K_PCG_DIRECTION, K_PCG_RUPDATE, K_PCG_POSTSWEEP, K_REDUCE) = range(11)
 LINEAR, INJECTION = 0, 1
 SUMMATION, TRANSPOSE = 0, 1
 OK, E_CONFIG, E_SHAPE, E_NONFINITE, E_FINGERPRINT, E_SINGULAR, E_CAP, E_CUDA, E_NCCL = range(9)

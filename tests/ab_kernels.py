@@ -11,7 +11,8 @@ from paper_1408_2981_b200 import synth, tpmg  # noqa: E402
 
 KERNELS = {"apply": tpmg.K_APPLY, "jacobi": tpmg.K_JACOBI, "jacobi0": tpmg.K_JACOBI_ZERO,
            "rr": tpmg.K_RESID_RESTRICT, "prolong": tpmg.K_PROLONG_ADD, "resid": tpmg.K_RESIDUAL,
-           "ap": tpmg.K_PCG_DIRECTION, "rupdate": tpmg.K_PCG_RUPDATE, "restrict": tpmg.K_RESTRICT}
+           "ap": tpmg.K_PCG_DIRECTION, "rupdate": tpmg.K_PCG_RUPDATE, "restrict": tpmg.K_RESTRICT,
+           "post": tpmg.K_PCG_POSTSWEEP}
 
 
 def main():
