@@ -137,6 +137,15 @@ int tpmg_abi_version(void);
 /* Fills 128 bytes with a fresh ncclUniqueId (rank 0 calls this, then broadcasts). */
 int tpmg_nccl_unique_id(void* out128);
 int tpmg_init(const tpmg_context_params* params, tpmg_context* out);
+/* The same context with the CUDA-IPC transport instead of NCCL: the ranks of one node (on
+ * distinct GPUs, or several processes sharing one GPU) write their halo faces straight into the
+ * neighbours' receive buffers (cudaIpcMemHandle mappings, exchanged at hierarchy creation) and
+ * reduce dot products in rank order through the POSIX shared-memory segment "/tpmg_<session>"
+ * (rank 0 creates it; every rank passes the same session string; removed once all attached).
+ * Each exchange and reduction is ordered by host barriers around stream synchronisations -- no
+ * kernel waits on another rank -- so iterations are not captured into CUDA graphs.  Hierarchy
+ * creation and destruction are collective.  world_size >= 2; nccl_id is ignored. */
+int tpmg_init_ipc(const tpmg_context_params* params, const char* session, tpmg_context* out);
 int tpmg_finalize(tpmg_context ctx);
 const char* tpmg_last_error(tpmg_context ctx);
 /* The cudaStream_t every call of this context is ordered on (for external CUDA-event timing). */

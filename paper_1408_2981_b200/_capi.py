@@ -21,6 +21,7 @@ SIGNATURES = {
     "tpmg_abi_version": (C.c_int, []),
     "tpmg_nccl_unique_id": (C.c_int, [C.c_void_p]),
     "tpmg_init": (C.c_int, [C.c_void_p, C.POINTER(_VP)]),
+    "tpmg_init_ipc": (C.c_int, [C.c_void_p, C.c_char_p, C.POINTER(_VP)]),
     "tpmg_finalize": (C.c_int, [_VP]),
     "tpmg_last_error": (C.c_char_p, [_VP]),
     "tpmg_context_stream": (C.c_int, [_VP, C.POINTER(C.c_void_p)]),

@@ -11,7 +11,14 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <fcntl.h>
+#include <sched.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -90,6 +97,22 @@ Nccl g_nccl;
 
 thread_local std::string g_global_error;
 
+// ---- CUDA-IPC transport (tpmg_init_ipc) ----------------------------------------------------
+// Ranks of one node (any GPUs, or several processes sharing one GPU) exchange halos by writing
+// straight into their neighbours' receive buffers (cudaIpcMemHandle mappings) and reduce their
+// dot products through a POSIX shared-memory segment.  Every step is ordered by HOST barriers
+// in that segment around stream synchronisations: no kernel ever waits on another rank.
+constexpr int kIpcMaxRanks = 64, kIpcMaxLevels = 24;
+constexpr uint64_t kIpcMagic = 0x31637069676d7074ull;  // "tpmgipc1"
+struct IpcShm {
+  std::atomic<uint64_t> magic;
+  std::atomic<uint32_t> count, gen, abort;
+  int32_t world;
+  double vals[2][kIpcMaxRanks];  // per-rank contributions, alternating phases
+  cudaIpcMemHandle_t handles[kIpcMaxRanks][kIpcMaxLevels][2];  // receive buffers per level / set
+};
+static_assert(std::atomic<uint32_t>::is_always_lock_free, "process-shared atomics");
+
 }  // namespace
 
 // ---- handles ------------------------------------------------------------------------------
@@ -98,6 +121,10 @@ struct tpmg_context_s {
   int rank = 0, world = 1, px = 1, py = 1, rx = 0, ry = 0;
   cudaStream_t stream = nullptr;
   ncclComm_t comm = nullptr;
+  // CUDA-IPC transport (tpmg_init_ipc): shared segment, reduction phase, pinned staging
+  IpcShm* ipc = nullptr;
+  int ipc_phase = 0;
+  double* ipc_host = nullptr;
   std::string last_error;
   int64_t launches = 0;
   tpmg::Launch launch() { return tpmg::Launch{stream, &launches}; }
@@ -152,6 +179,9 @@ struct Level {
   DevBuf u, t, f;              // V-cycle work: home iterate, ping-pong partner, rhs
   DevBuf send, recv;           // multi-GPU face buffers [W|E|S|N]
   DevBuf send2, recv2;         // finest level: a second set (z and p_old before the fused A p)
+  // IPC transport: where this rank's W / E / S / N faces land in the neighbours' receive
+  // buffers (per halo set)
+  double* peer[2][4] = {{nullptr, nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr, nullptr}};
   DevBuf d_piv, d_cpt;         // coarse levels: pre-factorised column blocks (LevelCoef::piv)
   LevelCoef coef(int nz) const {
     LevelCoef c;
@@ -231,6 +261,7 @@ struct tpmg_hierarchy_s {
   Probe probes[kProbes];
   uint32_t probe_pending = 0;  // pairs recorded by the work queued since the last collection
   std::unordered_map<const void*, uint32_t> iter_graph_probes;
+  std::vector<void*> ipc_mapped;  // neighbours' receive buffers opened through CUDA IPC
   int finest() const { return (int)lv.size() - 1; }
   VertCoef vcoef() const {
     VertCoef v{d_bv.p, d_sv.p, d_av.p, d_xv.p};
@@ -268,6 +299,48 @@ struct tpmg_hierarchy_s {
 };
 
 bool tpmg_hierarchy_s::multi() const { return ctx->world > 1 || loopback; }
+
+namespace {
+
+// host barrier of the IPC ranks (sense by generation count); a rank that fails or times out
+// raises the abort flag so the others fail instead of waiting forever
+void ipc_barrier(tpmg_context ctx) {
+  IpcShm* S = ctx->ipc;
+  const uint32_t g = S->gen.load(std::memory_order_acquire);
+  if (S->count.fetch_add(1, std::memory_order_acq_rel) + 1 == (uint32_t)ctx->world) {
+    S->count.store(0, std::memory_order_relaxed);
+    S->gen.fetch_add(1, std::memory_order_acq_rel);
+    return;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int spin = 0; S->gen.load(std::memory_order_acquire) == g; ++spin) {
+    if (S->abort.load(std::memory_order_relaxed))
+      throw Error(TPMG_E_NCCL, "ipc transport: another rank failed");
+    if (spin > 64) sched_yield();
+    if ((spin & 1023) == 0 &&
+        std::chrono::steady_clock::now() - t0 > std::chrono::seconds(120)) {
+      S->abort.store(1);
+      throw Error(TPMG_E_NCCL, "ipc transport: barrier timeout (a rank is missing)");
+    }
+  }
+}
+
+// sum (or max) of one double over the ranks, in rank order 0..world-1 on every rank
+double ipc_allreduce(tpmg_context ctx, double v, bool max_op) {
+  IpcShm* S = ctx->ipc;
+  const int ph = ctx->ipc_phase;
+  ctx->ipc_phase ^= 1;
+  S->vals[ph][ctx->rank] = v;
+  ipc_barrier(ctx);
+  double acc = S->vals[ph][0];
+  for (int r = 1; r < ctx->world; ++r) {
+    const double x = S->vals[ph][r];
+    acc = max_op ? (x > acc ? x : acc) : acc + x;
+  }
+  return acc;
+}
+
+}  // namespace
 
 struct tpmg_field_s {
   tpmg_hierarchy h = nullptr;
@@ -356,7 +429,20 @@ Halo exchange(tpmg_hierarchy h, int l, const double* u, int set = 0) {
   double* rE = rW + nwe;
   double* rS = rE + nwe;
   double* rN = rS + nsn;
-  if (h->loopback) {  // this rank is its own neighbour on every side
+  if (ctx->ipc) {
+    // the neighbours' kernels reading their receive buffers are done (barrier after each
+    // rank's stream drained), then every rank writes its faces into them, then all land
+    CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    ipc_barrier(ctx);
+    const double* src[4] = {sW, sE, sS, sN};
+    const int64_t cnt[4] = {nwe, nwe, nsn, nsn};
+    for (int d = 0; d < 4; ++d)
+      if ((d < 2 ? ctx->px : ctx->py) > 1)
+        CUDA_CHECK(cudaMemcpyAsync(L.peer[set][d], src[d], cnt[d] * 8, cudaMemcpyDeviceToDevice,
+                                   ctx->stream));
+    CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    ipc_barrier(ctx);
+  } else if (h->loopback) {  // this rank is its own neighbour on every side
     CUDA_CHECK(cudaMemcpyAsync(rE, sW, nwe * 8, cudaMemcpyDeviceToDevice, ctx->stream));
     CUDA_CHECK(cudaMemcpyAsync(rW, sE, nwe * 8, cudaMemcpyDeviceToDevice, ctx->stream));
     CUDA_CHECK(cudaMemcpyAsync(rN, sS, nsn * 8, cudaMemcpyDeviceToDevice, ctx->stream));
@@ -398,9 +484,18 @@ void finish_dot(tpmg_hierarchy h, int nblocks, int slot) {
   probe_begin(h, TPMG_K_REDUCE);
   tpmg::launch_reduce(ctx->launch(), h->partials.p, nblocks, h->scal.p + slot);
   probe_end(h, TPMG_K_REDUCE);
-  if (ctx->world > 1)
+  if (ctx->ipc) {
+    CUDA_CHECK(cudaMemcpyAsync(ctx->ipc_host, h->scal.p + slot, sizeof(double),
+                               cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    ctx->ipc_host[1] = ipc_allreduce(ctx, ctx->ipc_host[0], false);
+    CUDA_CHECK(cudaMemcpyAsync(h->scal.p + slot, ctx->ipc_host + 1, sizeof(double),
+                               cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  } else if (ctx->world > 1) {
     NCCL_CHECK(g_nccl.AllReduce(h->scal.p + slot, h->scal.p + slot, 1, ncclDouble, ncclSum,
                                 ctx->comm, ctx->stream));
+  }
 }
 
 // ---- kernel probes ----------------------------------------------------------------------
@@ -615,9 +710,17 @@ void sync_check(tpmg_hierarchy h) {
   int* h_err = reinterpret_cast<int*>(h->h_scal + 7);
   // multi-rank: every rank must take the same exit decision, or the ranks that did not see a
   // zero pivot would enter the next iteration's collectives alone and hang
-  if (h->ctx->world > 1)
+  if (h->ctx->ipc) {
+    int e = 0;
+    CUDA_CHECK(cudaMemcpyAsync(&e, h->d_err, sizeof(int), cudaMemcpyDeviceToHost, h->ctx->stream));
+    CUDA_CHECK(cudaStreamSynchronize(h->ctx->stream));
+    const int any = (int)ipc_allreduce(h->ctx, (double)e, true);
+    CUDA_CHECK(cudaMemcpyAsync(h->d_err, &any, sizeof(int), cudaMemcpyHostToDevice, h->ctx->stream));
+    CUDA_CHECK(cudaStreamSynchronize(h->ctx->stream));
+  } else if (h->ctx->world > 1) {
     NCCL_CHECK(g_nccl.AllReduce(h->d_err, h->d_err, 1, ncclInt32, ncclMax, h->ctx->comm,
                                 h->ctx->stream));
+  }
   CUDA_CHECK(cudaMemcpyAsync(h_err, h->d_err, sizeof(int), cudaMemcpyDeviceToHost,
                              h->ctx->stream));
   CUDA_CHECK(cudaStreamSynchronize(h->ctx->stream));
@@ -699,7 +802,7 @@ void run_iteration(tpmg_hierarchy h, double* x, bool first) {
   const int pc = h->pcur;
   // the fused A p pass moves the direction to the other buffer
   if (h->pcg_fused && h->fused_ap && !first) h->pcur ^= 1;
-  if (!h->use_graphs || (first && h->pcg_fused)) {
+  if (!h->use_graphs || ctx->ipc || (first && h->pcg_fused)) {  // IPC: host-ordered exchanges
     pcg_iteration(h, x, first, pc);
     return;
   }
@@ -880,8 +983,78 @@ int tpmg_init(const tpmg_context_params* prm, tpmg_context* out) {
   });
 }
 
+int tpmg_init_ipc(const tpmg_context_params* prm, const char* session, tpmg_context* out) {
+  return guard(nullptr, [&] {
+    if (!prm || !out || !session || !*session) throw Error(TPMG_E_CONFIG, "null argument");
+    if (prm->world_size < 2 || prm->world_size > kIpcMaxRanks || prm->rank < 0 ||
+        prm->rank >= prm->world_size)
+      throw Error(TPMG_E_CONFIG, "ipc transport: bad rank / world_size (2..64 ranks)");
+    if (prm->px * prm->py != prm->world_size)
+      throw Error(TPMG_E_CONFIG, "process grid px*py must equal world_size");
+    for (const char* c = session; *c; ++c)
+      if (*c == '/') throw Error(TPMG_E_CONFIG, "ipc transport: session name must not contain '/'");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      throw Error(TPMG_E_CUDA, "no CUDA device: the TPMG hot path has no CPU fallback");
+    auto ctx = std::make_unique<tpmg_context_s>();
+    if (prm->device >= 0) CUDA_CHECK(cudaSetDevice(prm->device));
+    CUDA_CHECK(cudaGetDevice(&ctx->device));
+    ctx->rank = prm->rank;
+    ctx->world = prm->world_size;
+    ctx->px = prm->px;
+    ctx->py = prm->py;
+    ctx->rx = prm->rank % prm->px;
+    ctx->ry = prm->rank / prm->px;
+    CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    tpmg::init_device_constants(ctx->stream);
+    CUDA_CHECK(cudaMallocHost(&ctx->ipc_host, 2 * sizeof(double)));
+    const std::string name = std::string("/tpmg_") + session;
+    const size_t bytes = sizeof(IpcShm);
+    int fd = -1;
+    if (ctx->rank == 0) {
+      shm_unlink(name.c_str());
+      fd = shm_open(name.c_str(), O_CREAT | O_EXCL | O_RDWR, 0600);
+      if (fd < 0 || ftruncate(fd, (off_t)bytes) != 0)
+        throw Error(TPMG_E_NCCL, "ipc transport: cannot create " + name);
+    } else {
+      const auto t0 = std::chrono::steady_clock::now();
+      while ((fd = shm_open(name.c_str(), O_RDWR, 0600)) < 0) {
+        if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(120))
+          throw Error(TPMG_E_NCCL, "ipc transport: rank 0 never created " + name);
+        usleep(1000);
+      }
+      struct stat st {};
+      while (fstat(fd, &st) == 0 && (size_t)st.st_size < bytes) usleep(1000);
+    }
+    void* m = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    close(fd);
+    if (m == MAP_FAILED) throw Error(TPMG_E_NCCL, "ipc transport: mmap failed");
+    ctx->ipc = static_cast<IpcShm*>(m);
+    if (ctx->rank == 0) {
+      ctx->ipc->count.store(0);
+      ctx->ipc->gen.store(0);
+      ctx->ipc->abort.store(0);
+      ctx->ipc->world = ctx->world;
+      ctx->ipc->magic.store(kIpcMagic, std::memory_order_release);
+    } else {
+      const auto t0 = std::chrono::steady_clock::now();
+      while (ctx->ipc->magic.load(std::memory_order_acquire) != kIpcMagic) {
+        if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(120))
+          throw Error(TPMG_E_NCCL, "ipc transport: segment never initialised");
+        usleep(1000);
+      }
+      if (ctx->ipc->world != ctx->world) throw Error(TPMG_E_CONFIG, "ipc transport: world mismatch");
+    }
+    ipc_barrier(ctx.get());                       // every rank has mapped the segment
+    if (ctx->rank == 0) shm_unlink(name.c_str());  // nothing left behind in /dev/shm
+    *out = ctx.release();
+  });
+}
+
 int tpmg_finalize(tpmg_context ctx) {
   if (!ctx) return TPMG_OK;
+  if (ctx->ipc) munmap(ctx->ipc, sizeof(IpcShm));
+  if (ctx->ipc_host) cudaFreeHost(ctx->ipc_host);
   if (ctx->comm) g_nccl.CommDestroy(ctx->comm);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -922,11 +1095,56 @@ int tpmg_plan_decomposition(int64_t nx, int64_t ny, int px, int py, int rank, in
 }
 
 namespace {
+// IPC transport: publish this rank's receive buffers, map the neighbours' (every rank builds
+// the same level structure, so the neighbour's buffers have this rank's shapes), and point
+// each face at the segment it must land in (W face -> west's E segment, and so on).
+void ipc_connect(tpmg_hierarchy h) {
+  tpmg_context ctx = h->ctx;
+  IpcShm* S = ctx->ipc;
+  const int nl = (int)h->lv.size();
+  if (nl > kIpcMaxLevels) throw Error(TPMG_E_CONFIG, "ipc transport: too many levels");
+  for (int l = 0; l < nl; ++l)
+    for (int set = 0; set < 2; ++set) {
+      const double* b = set ? h->lv[l].recv2.p : h->lv[l].recv.p;
+      if (b) CUDA_CHECK(cudaIpcGetMemHandle(&S->handles[ctx->rank][l][set], (void*)b));
+    }
+  ipc_barrier(ctx);
+  std::unordered_map<int64_t, double*> opened;
+  auto base = [&](int r, int l, int set) {
+    const int64_t key = ((int64_t)r * kIpcMaxLevels + l) * 2 + set;
+    auto it = opened.find(key);
+    if (it != opened.end()) return it->second;
+    void* p = nullptr;
+    CUDA_CHECK(cudaIpcOpenMemHandle(&p, S->handles[r][l][set], cudaIpcMemLazyEnablePeerAccess));
+    h->ipc_mapped.push_back(p);
+    return opened[key] = static_cast<double*>(p);
+  };
+  const int west = ctx->rank_of(ctx->rx - 1, ctx->ry), east = ctx->rank_of(ctx->rx + 1, ctx->ry);
+  const int south = ctx->rank_of(ctx->rx, ctx->ry - 1), north = ctx->rank_of(ctx->rx, ctx->ry + 1);
+  for (int l = 0; l < nl; ++l) {
+    Level& L = h->lv[l];
+    const int64_t nwe = (int64_t)L.ny * h->nz, nsn = (int64_t)L.nx * h->nz;
+    for (int set = 0; set < 2; ++set) {
+      if (!(set ? L.recv2.p : L.recv.p)) continue;
+      if (ctx->px > 1) {
+        L.peer[set][0] = base(west, l, set) + nwe;  // -> west's E segment
+        L.peer[set][1] = base(east, l, set);        // -> east's W segment
+      }
+      if (ctx->py > 1) {
+        L.peer[set][2] = base(south, l, set) + 2 * nwe + nsn;  // -> south's N segment
+        L.peer[set][3] = base(north, l, set) + 2 * nwe;        // -> north's S segment
+      }
+    }
+  }
+  ipc_barrier(ctx);
+}
+
 // build_hierarchy_coefficients (multigrid.hpp:242-272) for the three profile kinds of the
 // reference's ProfileVariant (multigrid.hpp:102-103): factorised `p`; partial = `p` with
 // alpha_r dense (`ar`, MixedProfileSet); full `fp` (ProfileSet).  Dense profiles are restricted
 // level by level exactly like the factorised horizontal scalars (restrict_profiles,
 // multigrid.hpp:146-201) and assembled per level (assemble_hatted, discretization.hpp:104-141,
+
 // 187-204) into [k][y][x] device arrays.
 int hier_create_impl(tpmg_context ctx, const tpmg_grid_desc* g, const tpmg_factorized_profiles* p,
                      const tpmg_full_profiles* fp, const double* ar, double omega,
@@ -1268,6 +1486,7 @@ int hier_create_impl(tpmg_context ctx, const tpmg_grid_desc* g, const tpmg_facto
       const char* e4 = getenv("TPMG_Q_IN_SWEEP");
       h->q_in_sweep = h->fused_ap && !(e4 && atoi(e4) == 0);
     }
+    if (ctx->ipc) ipc_connect(h.get());
     *out = h.release();
   });
 }
@@ -1397,6 +1616,13 @@ int tpmg_hier_coef_mode(tpmg_hierarchy h, int* mode) {
 int tpmg_hier_destroy(tpmg_hierarchy h) {
   if (!h) return TPMG_OK;
   cudaStreamSynchronize(h->ctx->stream);
+  if (h->ctx->ipc) {  // collective: unmap the neighbours' buffers before anyone frees its own
+    for (void* p : h->ipc_mapped) cudaIpcCloseMemHandle(p);
+    try {
+      ipc_barrier(h->ctx);
+    } catch (const Error&) {
+    }
+  }
   delete h;
   return TPMG_OK;
 }

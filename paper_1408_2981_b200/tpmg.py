@@ -80,14 +80,21 @@ class Context:
     """One GPU (rank) -- tpmg_init / tpmg_finalize."""
 
     def __init__(self, device: int = 0, rank: int = 0, world_size: int = 1, px: int = 1,
-                 py: int = 1, nccl_id: bytes | None = None, variant: str = "exact"):
+                 py: int = 1, nccl_id: bytes | None = None, variant: str = "exact",
+                 ipc_session: str | None = None):
+        """One rank.  world_size > 1: NCCL transport (nccl_id from rank 0), or with
+        `ipc_session` the CUDA-IPC transport (tpmg_init_ipc; every rank passes the same
+        session string)."""
         self.lib = _capi.load(variant)
         self._idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id else None
         prm = ContextParams(device, rank, world_size, px, py,
                             C.cast(self._idbuf, C.c_void_p) if self._idbuf else None)
         h = C.c_void_p()
         self._h = None
-        self._check(self.lib.tpmg_init(C.byref(prm), C.byref(h)))
+        if ipc_session:
+            self._check(self.lib.tpmg_init_ipc(C.byref(prm), ipc_session.encode(), C.byref(h)))
+        else:
+            self._check(self.lib.tpmg_init(C.byref(prm), C.byref(h)))
         self._h = h
         self.rank, self.world_size, self.px, self.py = rank, world_size, px, py
 
