@@ -453,6 +453,13 @@ double column_reduce(const DevOrder& d, const std::vector<double>& colsum, int n
   return reduce_partials(part);
 }
 
+// dot_into of the device (tpmg_host.cpp): k_dot_tiles on a level that tiles by 32x4 (per-thread
+// column sums over k, per-tile block tree, k_reduce), k_dot's grid-stride tree otherwise
+double tile_or_gridstride_dot(const DevOrder& d, const double* a, const double* b) {
+  if (d.nx % 32 == 0 && d.ny % 4 == 0) return column_dot(d, a, b);
+  return gridstride_dot(d, [&](Index i) { return a[i] * b[i]; });
+}
+
 void check_finite(const double* p, Index n, const char* what) {
   for (Index i = 0; i < n; ++i)
     if (!std::isfinite(p[i])) throw Error(E_NONFINITE, std::string("non-finite values in ") + what);
@@ -1002,9 +1009,15 @@ int tpmgo_pcg_timed(tpmgo_hier H, const double* f, double* x, double tol, int ma
       for (double v : part) s += v;
       return s;
     };
+    // the device's dot_into: tile-layout dot (k_dot_tiles) on a tiled level, else k_dot
     auto dotv = [&](const std::vector<double>& a, const std::vector<double>& b) {
-      return dev ? gridstride_dot(d, [&](Index i) { return a[i] * b[i]; })
+      return dev ? tile_or_gridstride_dot(d, a.data(), b.data())
                  : (h.device_order ? dot(n, a.data(), b.data()) : pdot(a.data(), b.data()));
+    };
+    // k_pcg_xr (the unfused schedule's |r|^2): grid-stride partials
+    auto gsdot = [&](const std::vector<double>& a) {
+      return dev ? gridstride_dot(d, [&](Index i) { return a[i] * a[i]; })
+                 : (h.device_order ? dot(n, a.data(), a.data()) : pdot(a.data(), a.data()));
     };
     // The device fuses |r|^2 into the first and r.z into the last finest-level sweep when the
     // finest level runs the tiled TMEM smoother (tpmg_host.cpp pcg_iteration); those partials
@@ -1050,7 +1063,7 @@ int tpmgo_pcg_timed(tpmgo_hier H, const double* f, double* x, double tol, int ma
           r[i] -= alpha * q[i];
         }
       });
-      const double rn = std::sqrt(fused ? column_dot(d, r.data(), r.data(), false, nc) : dotv(r, r));
+      const double rn = std::sqrt(fused ? column_dot(d, r.data(), r.data(), false, nc) : gsdot(r));
       if (res_hist) res_hist[it] = rn;
       *iters = it;
       stamp(it);
@@ -1097,7 +1110,7 @@ struct Outer {
       : h(hh), L(static_cast<int>(hh.lv.size()) - 1), n(hh.lv[L].ncells * hh.nz),
         dev(hh.cart_nx > 0 && hh.device_order), d{hh.cart_nx, hh.cart_ny, hh.nz} {}
   double dotv(const std::vector<double>& a, const std::vector<double>& b) const {
-    return dev ? gridstride_dot(d, [&](Index i) { return a[i] * b[i]; }) : dot(n, a.data(), b.data());
+    return dev ? tile_or_gridstride_dot(d, a.data(), b.data()) : dot(n, a.data(), b.data());
   }
   // M^{-1} r: mu V-cycles on A e = r from e = 0
   void precond(int mu, const std::vector<double>& r, std::vector<double>& e) const {

@@ -62,6 +62,8 @@ struct Nccl {
   ncclResult_t (*GroupEnd)() = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 
   void load() {
@@ -83,6 +85,7 @@ struct Nccl {
     GroupStart = (decltype(GroupStart))sym("ncclGroupStart");
     GroupEnd = (decltype(GroupEnd))sym("ncclGroupEnd");
     AllReduce = (decltype(AllReduce))sym("ncclAllReduce");
+    AllGather = (decltype(AllGather))sym("ncclAllGather");
     GetErrorString = (decltype(GetErrorString))sym("ncclGetErrorString");
   }
 };
@@ -103,12 +106,14 @@ thread_local std::string g_global_error;
 // dot products through a POSIX shared-memory segment.  Every step is ordered by HOST barriers
 // in that segment around stream synchronisations: no kernel ever waits on another rank.
 constexpr int kIpcMaxRanks = 64, kIpcMaxLevels = 24;
+constexpr int kIpcGatherMax = 32768;  // tile partials per rank (tiles up to 2048 x 2048 columns)
 constexpr uint64_t kIpcMagic = 0x31637069676d7074ull;  // "tpmgipc1"
 struct IpcShm {
   std::atomic<uint64_t> magic;
   std::atomic<uint32_t> count, gen, abort;
   int32_t world;
   double vals[2][kIpcMaxRanks];  // per-rank contributions, alternating phases
+  double gather[2][kIpcMaxRanks][kIpcGatherMax];  // per-rank tile partials, alternating phases
   cudaIpcMemHandle_t handles[kIpcMaxRanks][kIpcMaxLevels][2];  // receive buffers per level / set
 };
 static_assert(std::atomic<uint32_t>::is_always_lock_free, "process-shared atomics");
@@ -224,6 +229,7 @@ struct tpmg_hierarchy_s {
   int64_t n_precond = 0, n_matvec = 0;
   double* pbuf(int i) { return i == 0 ? p.p : p2.p; }
   DevBuf partials, scal;  // reduction partials; scalars s[0..7]
+  DevBuf gathered;        // multi-rank: every rank's tile partials (gather_partials)
   int* d_err = nullptr;
   double* h_scal = nullptr;  // pinned
   bool use_graphs = true;
@@ -479,8 +485,47 @@ Halo exchange(tpmg_hierarchy h, int l, const double* u, int set = 0) {
 // s[slot] = global sum of the per-block partials.
 void probe_begin(tpmg_hierarchy h, int id);
 void probe_end(tpmg_hierarchy h, int id);
-void finish_dot(tpmg_hierarchy h, int nblocks, int slot) {
+// every rank's `nb` partials into h->gathered, rank r at r*nb
+void gather_partials(tpmg_hierarchy h, int nb) {
   tpmg_context ctx = h->ctx;
+  if ((int64_t)nb * ctx->world > (int64_t)h->gathered.n)
+    throw Error(TPMG_E_CAP, "gather buffer too small");
+  if (ctx->ipc) {  // through the shared segment (phase alternation as in ipc_allreduce)
+    IpcShm* S = ctx->ipc;
+    if (nb > kIpcGatherMax) throw Error(TPMG_E_CAP, "ipc transport: too many tile partials");
+    const int ph = ctx->ipc_phase;
+    ctx->ipc_phase ^= 1;
+    CUDA_CHECK(cudaMemcpyAsync(S->gather[ph][ctx->rank], h->partials.p, (size_t)nb * 8,
+                               cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    ipc_barrier(ctx);
+    for (int r = 0; r < ctx->world; ++r)
+      CUDA_CHECK(cudaMemcpyAsync(h->gathered.p + (int64_t)r * nb, S->gather[ph][r], (size_t)nb * 8,
+                                 cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  } else {
+    NCCL_CHECK(g_nccl.AllGather(h->partials.p, h->gathered.p, (size_t)nb, ncclDouble, ctx->comm,
+                                ctx->stream));
+  }
+}
+// s[slot] = global sum of the per-block partials.  `tile_level` >= 0: the partials are the
+// 32x4-tile partials of that level (k_dot_tiles / the fused kernels).  A decomposed run then
+// gathers every rank's tile partials and reduces them in the global tile order of a one-rank
+// run: the dot products -- and with them the whole PCG solve -- are bitwise independent of the
+// number of ranks.  Other layouts: local fixed-order sum, then a sum over the ranks.
+void finish_dot(tpmg_hierarchy h, int nblocks, int slot, int tile_level = -1) {
+  tpmg_context ctx = h->ctx;
+  if (ctx->world > 1 && tile_level >= 0) {
+    const Level& L = h->lv[tile_level];
+    if (tpmg::dot_tiles_ok(L.nx, L.ny) && nblocks == (L.nx / 32) * (L.ny / 4)) {
+      gather_partials(h, nblocks);
+      probe_begin(h, TPMG_K_REDUCE);
+      tpmg::launch_reduce_tiles(ctx->launch(), h->gathered.p, nblocks, L.nx / 32,
+                                L.ny / 4, ctx->px, ctx->py, h->scal.p + slot);
+      probe_end(h, TPMG_K_REDUCE);
+      return;
+    }
+  }
   probe_begin(h, TPMG_K_REDUCE);
   tpmg::launch_reduce(ctx->launch(), h->partials.p, nblocks, h->scal.p + slot);
   probe_end(h, TPMG_K_REDUCE);
@@ -535,10 +580,18 @@ void probe_collect(tpmg_hierarchy h) {
   h->probe_pending = 0;
 }
 
-void dot_into(tpmg_hierarchy h, int64_t n, const double* a, const double* b, int slot) {
+// a.b of two fields of level l: on a tiled Cartesian level in the fused kernels' tile layout
+// (k_dot_tiles), so that every PCG dot of a decomposed run reduces to the one-rank bits
+void dot_into(tpmg_hierarchy h, int l, const double* a, const double* b, int slot) {
+  Level& L = h->lv[l];
   int nb = 0;
-  tpmg::launch_dot(h->ctx->launch(), n, a, b, h->partials.p, &nb);
-  finish_dot(h, nb, slot);
+  if (!h->generic && tpmg::dot_tiles_ok(L.nx, L.ny)) {
+    tpmg::launch_dot_tiles(h->ctx->launch(), L.nx, L.ny, h->nz, a, b, h->partials.p, &nb);
+    finish_dot(h, nb, slot, l);
+  } else {
+    tpmg::launch_dot(h->ctx->launch(), L.plane * h->nz, a, b, h->partials.p, &nb);
+    finish_dot(h, nb, slot);
+  }
 }
 
 // ---- hot-path building blocks ------------------------------------------------------------
@@ -549,7 +602,7 @@ void apply_level(tpmg_hierarchy h, int l, int mode, const double* u, const doubl
   int nb = 0;
   tpmg::launch_apply(h->ctx->launch(), h->vcoef(), L.coef(h->nz), h->xi, mode, u, H, f, y,
                      dot_slot >= 0 ? h->partials.p : nullptr, &nb);
-  if (dot_slot >= 0) finish_dot(h, nb, dot_slot);
+  if (dot_slot >= 0) finish_dot(h, nb, dot_slot, l);
 }
 
 // One line-Jacobi sweep.  With `fz` the sweep also does fused PCG work (see PcgFuse) and its
@@ -566,7 +619,7 @@ void sweep(tpmg_hierarchy h, int l, const double* u_in, const double* f, double*
   tpmg::launch_jacobi(h->ctx->launch(), h->vcoef(), L.coef(h->nz), h->xi, u_in, H, f, out,
                       h->relax, h->d_err, fz, &nb, pro);
   if (probe >= 0) probe_end(h, probe);
-  if (fz) finish_dot(h, nb, slot);
+  if (fz) finish_dot(h, nb, slot, l);
 }
 
 // fine level lf -> coarse lf-1: coarse = R (f - A u).  `scratch` is a free fine-level buffer.
@@ -773,7 +826,7 @@ void pcg_iteration(tpmg_hierarchy h, double* x, bool first, int pc) {
                           h->q_in_sweep ? nullptr : h->q.p, x, h->scal.p, h->partials.p, &nb);
       probe_end(h, TPMG_K_PCG_DIRECTION);
       tpmg::launch_copy_scalar(ctx->launch(), h->scal.p, 0, 3);
-      finish_dot(h, nb, 1);
+      finish_dot(h, nb, 1, L);
       vcycle(h, L, h->r.p, h->z.p, h->tmp.p, true, true,
              h->q_in_sweep ? h->pbuf(pc ^ 1) : nullptr);
       return;
@@ -792,7 +845,7 @@ void pcg_iteration(tpmg_hierarchy h, double* x, bool first, int pc) {
   tpmg::launch_pcg_xr(ctx->launch(), n, h->scal.p, x, h->r.p, h->p.p, h->q.p, h->partials.p, &nb);
   finish_dot(h, nb, 2);
   vcycle(h, L, h->r.p, h->z.p, h->tmp.p, true);
-  dot_into(h, n, h->r.p, h->z.p, 3);
+  dot_into(h, L, h->r.p, h->z.p, 3);
   tpmg::launch_pcg_p(ctx->launch(), n, h->scal.p, h->z.p, h->p.p);
   tpmg::launch_copy_scalar(ctx->launch(), h->scal.p, 0, 3);
 }
@@ -1428,6 +1481,8 @@ int hier_create_impl(tpmg_context ctx, const tpmg_grid_desc* g, const tpmg_facto
     const int64_t nf = h->lv[levels - 1].plane * nz;
     h->r.alloc(nf); h->z.alloc(nf); h->p.alloc(nf); h->q.alloc(nf); h->tmp.alloc(nf);
     h->partials.alloc(std::max<int64_t>(max_blocks, 148 * 8));
+    if (ctx->world > 1)  // tile partials of the finest level, every rank's
+      h->gathered.alloc((size_t)ctx->world * (h->lv[levels - 1].plane / 128 + 1));
     h->scal.alloc(8);
     CUDA_CHECK(cudaMemsetAsync(h->scal.p, 0, 8 * sizeof(double), h->ctx->stream));
     CUDA_CHECK(cudaMalloc(&h->d_err, sizeof(int)));
@@ -1830,7 +1885,7 @@ int tpmg_dot(tpmg_hierarchy h, tpmg_field a, tpmg_field b, double* out) {
   return guard(h->ctx, [&] {
     same_hier(h, a); same_hier(h, b);
     if (a->level != b->level) throw Error(TPMG_E_SHAPE, "dot: shapes differ");
-    dot_into(h, a->buf.n, a->buf.p, b->buf.p, 4);
+    dot_into(h, a->level, a->buf.p, b->buf.p, 4);
     *out = read_scalar(h, 4);
   });
 }
@@ -1856,12 +1911,12 @@ int tpmg_measure_cycle_rate(tpmg_hierarchy h, tpmg_field f, int n_cycles, double
     for (int i = 1; i <= n_cycles; ++i) {
       vcycle(h, L, f->buf.p, u, h->tmp.p, i == 1);
       apply_level(h, L, tpmg::APPLY_RESID, u, f->buf.p, r);
-      dot_into(h, n, r, r, 5);
+      dot_into(h, L, r, r, 5);
       const double nrm = std::sqrt(read_scalar(h, 5));
       if (i == 1) first = nrm;
       last = nrm;
     }
-    dot_into(h, n, f->buf.p, f->buf.p, 5);
+    dot_into(h, L, f->buf.p, f->buf.p, 5);
     const double fn = std::sqrt(read_scalar(h, 5));
     if (first <= 1e-300 || first <= 2.220446049250313e-16 * fn) {
       *rate = 0.0;
@@ -1891,7 +1946,7 @@ int tpmg_pcg(tpmg_hierarchy h, tpmg_field f, tpmg_field x, double tol, int max_i
       CUDA_CHECK(cudaMemcpyAsync(h->r.p, f->buf.p, n * 8, cudaMemcpyDeviceToDevice, s));
       r0p = h->r.p;
     }
-    dot_into(h, n, r0p, r0p, 2);
+    dot_into(h, L, r0p, r0p, 2);
     const double r0 = std::sqrt(read_scalar(h, 2));
     if (res_hist) res_hist[0] = r0;
     *iters = 0;
@@ -1901,7 +1956,7 @@ int tpmg_pcg(tpmg_hierarchy h, tpmg_field f, tpmg_field x, double tol, int max_i
     // V-cycle writes z itself): no 1 GB device copy
     vcycle(h, L, r0p, h->p.p, h->tmp.p, true);
     h->pcur = 0;
-    dot_into(h, n, r0p, h->p.p, 0);
+    dot_into(h, L, r0p, h->p.p, 0);
     if (!(read_scalar(h, 0) > 0.0)) {
       *solve_status = TPMG_BREAKDOWN;
       return;
@@ -2009,7 +2064,8 @@ void precondition(tpmg_hierarchy h, int mu, const double* r, double* e) {
   ++h->n_precond;
 }
 double dot_now(tpmg_hierarchy h, int64_t n, const double* a, const double* b) {
-  dot_into(h, n, a, b, 4);
+  (void)n;  // finest-level fields
+  dot_into(h, h->finest(), a, b, 4);
   return read_scalar(h, 4);
 }
 }  // namespace

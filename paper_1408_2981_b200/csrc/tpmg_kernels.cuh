@@ -214,6 +214,14 @@ void launch_dot(const Launch& L, int64_t n, const double* a, const double* b, do
 // out[slot] = sum(partials[0..nblocks)) in fixed order; if copy_from >= 0 also s[copy_to] = s[copy_from]
 // first (used to roll rho_new -> rho).
 void launch_reduce(const Launch& L, const double* partials, int nblocks, double* out);
+// Tile-layout dot (32x4 columns per partial, the fused kernels' layout) on an nx x ny x nz
+// field; dot_tiles_ok: the level tiles.  launch_reduce_tiles: k_reduce over px x py ranks' tile
+// partials in the global tile order (bitwise the one-rank result).
+bool dot_tiles_ok(int nx, int ny);
+void launch_dot_tiles(const Launch& L, int nx, int ny, int nz, const double* a, const double* b,
+                      double* partials, int* nblocks);
+void launch_reduce_tiles(const Launch& L, const double* gathered, int64_t stride, int gxl,
+                         int gyl, int px, int py, double* out);
 void launch_copy_scalar(const Launch& L, double* s, int dst, int src);
 
 // Layout permutations for upload/download: k-fastest (reference Field) <-> [k][y][x].

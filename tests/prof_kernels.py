@@ -8,7 +8,8 @@ sys.path.insert(0, ROOT)
 from paper_1408_2981_b200 import synth, tpmg  # noqa: E402
 
 KERNELS = {"apply": tpmg.K_APPLY, "jacobi": tpmg.K_JACOBI, "jacobi0": tpmg.K_JACOBI_ZERO,
-           "rr": tpmg.K_RESID_RESTRICT, "prolong": tpmg.K_PROLONG_ADD, "resid": tpmg.K_RESIDUAL}
+           "rr": tpmg.K_RESID_RESTRICT, "prolong": tpmg.K_PROLONG_ADD, "resid": tpmg.K_RESIDUAL,
+           "post": tpmg.K_PCG_POSTSWEEP, "rupdate": tpmg.K_PCG_RUPDATE, "ap": tpmg.K_PCG_DIRECTION}
 
 
 def main():
