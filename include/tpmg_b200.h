@@ -233,6 +233,13 @@ int tpmg_restrict(tpmg_hierarchy h, tpmg_field fine, tpmg_field coarse);
 int tpmg_prolong_add(tpmg_hierarchy h, tpmg_field coarse, tpmg_field fine);
 /* prolongate_field alone: fine = P coarse. */
 int tpmg_prolong(tpmg_hierarchy h, tpmg_field coarse, tpmg_field fine);
+/* The reference's transfer entry points with an explicit kind, independent of the hierarchy's
+ * TransferConfig: restrict_field (TPMG_RESTRICT_SUMMATION, multigrid.hpp:29-43) /
+ * restrict_field_transpose (TPMG_RESTRICT_TRANSPOSE, :46-69); prolongate_field(..., kind)
+ * (:74-100), with add != 0 fine += P coarse. */
+int tpmg_restrict_kind(tpmg_hierarchy h, tpmg_field fine, tpmg_field coarse, int restriction);
+int tpmg_prolong_kind(tpmg_hierarchy h, tpmg_field coarse, tpmg_field fine, int prolongation,
+                      int add);
 /* v_cycle(m, finest, f, u), multigrid.hpp:276-299: one V-cycle, u updated in place. */
 int tpmg_vcycle(tpmg_hierarchy h, tpmg_field f, tpmg_field u);
 /* measure_cycle_rate, multigrid.hpp:302-321. */

@@ -27,6 +27,16 @@ def main() -> int:
     subprocess.run(cmd, check=True)
     data = os.path.join(OUT, "ref_pin.bin")
     subprocess.run([exe, data], check=True)
+    # the drop-in adapter driver: the reference's own objects handed to the device through
+    # include/tpmg_b200_ref.hpp (run on the GPU box by tests/test_ref_adapter_gpu.py)
+    lib_dir = os.path.join(ROOT, "paper_1408_2981_b200")
+    if os.path.exists(os.path.join(lib_dir, "libtpmg_b200.so")):
+        cmd = ["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-I", os.path.join(HERE, "eigen_shim"),
+               "-I", REF_INC, "-I", os.path.join(ROOT, "include"),
+               os.path.join(HERE, "ref_adapter_driver.cpp"), "-o",
+               os.path.join(OUT, "ref_adapter_driver"), "-L", lib_dir, "-ltpmg_b200",
+               "-Wl,-rpath,$ORIGIN/../../paper_1408_2981_b200"]
+        subprocess.run(cmd, check=True)
     golden = os.path.join(ROOT, "tests", "golden", "ref_icosa_pin.bin")
     os.makedirs(os.path.dirname(golden), exist_ok=True)
     shutil.copyfile(data, golden)

@@ -623,7 +623,7 @@ void sweep(tpmg_hierarchy h, int l, const double* u_in, const double* f, double*
 }
 
 // fine level lf -> coarse lf-1: coarse = R (f - A u).  `scratch` is a free fine-level buffer.
-void restrict_plain(tpmg_hierarchy h, int lf, const double* fine, double* coarse);
+void restrict_plain(tpmg_hierarchy h, int lf, const double* fine, double* coarse, int kind);
 
 void resid_restrict(tpmg_hierarchy h, int lf, const double* u, const double* f, double* coarse,
                     double* scratch, bool probe = false) {
@@ -631,7 +631,7 @@ void resid_restrict(tpmg_hierarchy h, int lf, const double* u, const double* f, 
   Level& C = h->lv[lf - 1];
   if (h->generic) {
     apply_level(h, lf, tpmg::APPLY_RESID, u, f, scratch);
-    restrict_plain(h, lf, scratch, coarse);
+    restrict_plain(h, lf, scratch, coarse, -1);
     return;
   }
   if (h->restriction == TPMG_RESTRICT_SUMMATION) {
@@ -650,15 +650,15 @@ void resid_restrict(tpmg_hierarchy h, int lf, const double* u, const double* f, 
   }
 }
 
-void restrict_plain(tpmg_hierarchy h, int lf, const double* fine, double* coarse) {
+void restrict_plain(tpmg_hierarchy h, int lf, const double* fine, double* coarse, int kind = -1) {
   Level& C = h->lv[lf - 1];
+  if (kind < 0) kind = h->restriction;
   if (h->generic) {
     tpmg::launch_restrict_gen(h->ctx->launch(), C.coef(h->nz), C.d_children.p, h->rule,
-                              h->lv[lf].plane, fine, coarse,
-                              h->restriction == TPMG_RESTRICT_TRANSPOSE);
+                              h->lv[lf].plane, fine, coarse, kind == TPMG_RESTRICT_TRANSPOSE);
     return;
   }
-  if (h->restriction == TPMG_RESTRICT_SUMMATION) {
+  if (kind == TPMG_RESTRICT_SUMMATION) {
     tpmg::launch_restrict_sum(h->ctx->launch(), C.nx, C.ny, h->nz, fine, coarse);
   } else {
     const Halo Hf = exchange(h, lf, fine);
@@ -667,9 +667,9 @@ void restrict_plain(tpmg_hierarchy h, int lf, const double* fine, double* coarse
 }
 
 void prolong_level(tpmg_hierarchy h, int lc, const double* coarse, double* fine, bool add,
-                   bool probe = false) {
+                   bool probe = false, int kind = -1) {
   Level& F = h->lv[lc + 1];
-  const bool linear = h->prolongation == TPMG_PROLONG_LINEAR;
+  const bool linear = (kind < 0 ? h->prolongation : kind) == TPMG_PROLONG_LINEAR;
   if (h->generic) {
     Level& C = h->lv[lc];
     tpmg::launch_prolong_gen(h->ctx->launch(), C.coef(h->nz), C.d_children.p, h->rule, F.plane,
@@ -1848,7 +1848,7 @@ int tpmg_restrict(tpmg_hierarchy h, tpmg_field fine, tpmg_field coarse) {
     same_hier(h, fine); same_hier(h, coarse);
     if (fine->level != coarse->level + 1)
       throw Error(TPMG_E_SHAPE, "restrict_field: fine field is not one level above the target");
-    restrict_plain(h, fine->level, fine->buf.p, coarse->buf.p);
+    restrict_plain(h, fine->level, fine->buf.p, coarse->buf.p, -1);
     sync_check(h);
   });
 }
@@ -1859,6 +1859,31 @@ static int prolong_impl(tpmg_hierarchy h, tpmg_field coarse, tpmg_field fine, bo
     if (fine->level != coarse->level + 1)
       throw Error(TPMG_E_SHAPE, "prolongate_field: field level does not match");
     prolong_level(h, coarse->level, coarse->buf.p, fine->buf.p, add);
+    sync_check(h);
+  });
+}
+
+int tpmg_restrict_kind(tpmg_hierarchy h, tpmg_field fine, tpmg_field coarse, int restriction) {
+  return guard(h->ctx, [&] {
+    same_hier(h, fine); same_hier(h, coarse);
+    if (fine->level != coarse->level + 1)
+      throw Error(TPMG_E_SHAPE, "restrict_field: fine field is not one level above the target");
+    if (restriction != TPMG_RESTRICT_SUMMATION && restriction != TPMG_RESTRICT_TRANSPOSE)
+      throw Error(TPMG_E_CONFIG, "unknown restriction kind");
+    restrict_plain(h, fine->level, fine->buf.p, coarse->buf.p, restriction);
+    sync_check(h);
+  });
+}
+
+int tpmg_prolong_kind(tpmg_hierarchy h, tpmg_field coarse, tpmg_field fine, int prolongation,
+                      int add) {
+  return guard(h->ctx, [&] {
+    same_hier(h, fine); same_hier(h, coarse);
+    if (fine->level != coarse->level + 1)
+      throw Error(TPMG_E_SHAPE, "prolongate_field: field level does not match");
+    if (prolongation != TPMG_PROLONG_LINEAR && prolongation != TPMG_PROLONG_INJECTION)
+      throw Error(TPMG_E_CONFIG, "unknown prolongation kind");
+    prolong_level(h, coarse->level, coarse->buf.p, fine->buf.p, add != 0, false, prolongation);
     sync_check(h);
   });
 }
