@@ -97,7 +97,7 @@ def kernel_key(name):
     m = re.search(r"k_jacobi_t3<([^>]*)>", name)
     if m:
         a = [x.strip() for x in m.group(1).split(",")]
-        zero, pcgf = a[1] == "true", int(a[6])
+        zero, pcgf = a[1] in ("true", "1"), int(a[6])
         if pcgf == 2:
             return "pcg_postsweep_rz", 24 * N + 32 * C
         if pcgf == 3:
@@ -117,10 +117,25 @@ def kernel_key(name):
     return None, None
 
 
-def table(rep, out, peak=6558.4, json_out=None):
+def table(reps, out, peak=6558.4, json_out=None):
+    """`reps`: one report, or several separated by commas (one per kernel variant)."""
+    best = {}
+    for rep in reps.split(","):
+        _table_rows(rep, peak, best)
+    rep = reps
+    lines = _table_lines(rep, peak, best)
+    open(out, "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+    if json_out:
+        json.dump(best, open(json_out, "w"), indent=1)
+
+
+def _table_rows(rep, peak, best):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
+    if len(rows) < 3:
+        return
     hdr, units = rows[0], rows[1]
     col = {h: i for i, h in enumerate(hdr)}
 
@@ -133,7 +148,6 @@ def table(rep, out, peak=6558.4, json_out=None):
         return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3,
                     "usecond": 1, "msecond": 1e3}.get(u, 1)
 
-    best = {}
     for r in rows[2:]:
         key, alg = kernel_key(r[col["Kernel Name"]])
         if key is None:
@@ -155,6 +169,9 @@ def table(rep, out, peak=6558.4, json_out=None):
                "registers": num(r, "launch__registers_per_thread"),
                "l2_hit_pct": num(r, "lts__t_sector_hit_rate.pct"), "top_stalls": top, "source": rep}
         best[key] = rec  # the last launch of each variant (warm)
+
+
+def _table_lines(rep, peak, best):
     lines = [f"# ncu --set full, finest level of BASELINE config 3 (1024^2 x 128): `{rep}`", "",
              f"Algorithmic bytes per SURVEY.md §8(d); fraction = algorithmic bytes / ncu duration / "
              f"{peak} GB/s (measured copy peak). ncu serialises and flushes caches, so durations "
@@ -169,10 +186,7 @@ def table(rep, out, peak=6558.4, json_out=None):
                      f"{v['frac_of_peak']:.3f} | {f(v['fp64_pipe_pct'])}% | {f(v['issue_pct'])}% | "
                      f"{f(v['warps_active_pct'])}% | {f(v['registers'], 0)} | {f(v['l2_hit_pct'])}% | "
                      f"{v['top_stalls']} |")
-    open(out, "w").write("\n".join(lines) + "\n")
-    print("\n".join(lines))
-    if json_out:
-        json.dump(best, open(json_out, "w"), indent=1)
+    return lines
 
 
 if __name__ == "__main__":
