@@ -47,6 +47,8 @@ SIGNATURES = {
     "tpmg_restrict": (C.c_int, [_VP, _VP, _VP]),
     "tpmg_prolong_add": (C.c_int, [_VP, _VP, _VP]),
     "tpmg_prolong": (C.c_int, [_VP, _VP, _VP]),
+    "tpmg_restrict_kind": (C.c_int, [_VP, _VP, _VP, C.c_int]),
+    "tpmg_prolong_kind": (C.c_int, [_VP, _VP, _VP, C.c_int, C.c_int]),
     "tpmg_vcycle": (C.c_int, [_VP, _VP, _VP]),
     "tpmg_measure_cycle_rate": (C.c_int, [_VP, _VP, C.c_int, _D]),
     "tpmg_dot": (C.c_int, [_VP, _VP, _VP, _D]),

@@ -114,7 +114,7 @@ struct IpcShm {
   int32_t world;
   double vals[2][kIpcMaxRanks];  // per-rank contributions, alternating phases
   double gather[2][kIpcMaxRanks][kIpcGatherMax];  // per-rank tile partials, alternating phases
-  cudaIpcMemHandle_t handles[kIpcMaxRanks][kIpcMaxLevels][2];  // receive buffers per level / set
+  cudaIpcMemHandle_t handles[kIpcMaxRanks][kIpcMaxLevels][3];  // receive buffers per level / set
 };
 static_assert(std::atomic<uint32_t>::is_always_lock_free, "process-shared atomics");
 
@@ -184,9 +184,12 @@ struct Level {
   DevBuf u, t, f;              // V-cycle work: home iterate, ping-pong partner, rhs
   DevBuf send, recv;           // multi-GPU face buffers [W|E|S|N]
   DevBuf send2, recv2;         // finest level: a second set (z and p_old before the fused A p)
+  DevBuf send3, recv3;         // two-cell halo with corners (tpmg::Halo2 layout, fused R(f - A u))
+  DevBuf d_ringc;              // coefficient scalars on the 1-cell ring around the tile
   // IPC transport: where this rank's W / E / S / N faces land in the neighbours' receive
-  // buffers (per halo set)
+  // buffers (per halo set), and its deep pieces W, E, S, N, SW, SE, NW, NE
   double* peer[2][4] = {{nullptr, nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr, nullptr}};
+  double* peer3[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   DevBuf d_piv, d_cpt;         // coarse levels: pre-factorised column blocks (LevelCoef::piv)
   LevelCoef coef(int nz) const {
     LevelCoef c;
@@ -426,7 +429,6 @@ Halo exchange(tpmg_hierarchy h, int l, const double* u, int set = 0) {
   const bool xs = ctx->px > 1 || h->loopback, ys = ctx->py > 1 || h->loopback;
   const int nz = h->nz;
   const int64_t nwe = (int64_t)L.ny * nz, nsn = (int64_t)L.nx * nz;
-  tpmg::launch_pack_faces(ctx->launch(), L.nx, L.ny, nz, u, SB.p);
   double* sW = SB.p;
   double* sE = sW + nwe;
   double* sS = sE + nwe;
@@ -435,25 +437,25 @@ Halo exchange(tpmg_hierarchy h, int l, const double* u, int set = 0) {
   double* rE = rW + nwe;
   double* rS = rE + nwe;
   double* rN = rS + nsn;
+  // each face is packed straight to where it lands: this rank's own receive buffer (loopback:
+  // the periodic neighbour of a 1x1 process grid is the rank itself), the neighbour's receive
+  // buffer (CUDA-IPC peer mapping), or the send buffer NCCL transfers
   if (ctx->ipc) {
     // the neighbours' kernels reading their receive buffers are done (barrier after each
     // rank's stream drained), then every rank writes its faces into them, then all land
     CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
     ipc_barrier(ctx);
-    const double* src[4] = {sW, sE, sS, sN};
-    const int64_t cnt[4] = {nwe, nwe, nsn, nsn};
-    for (int d = 0; d < 4; ++d)
-      if ((d < 2 ? ctx->px : ctx->py) > 1)
-        CUDA_CHECK(cudaMemcpyAsync(L.peer[set][d], src[d], cnt[d] * 8, cudaMemcpyDeviceToDevice,
-                                   ctx->stream));
+    tpmg::FaceDst dst{{ctx->px > 1 ? L.peer[set][0] : nullptr, ctx->px > 1 ? L.peer[set][1] : nullptr,
+                       ctx->py > 1 ? L.peer[set][2] : nullptr, ctx->py > 1 ? L.peer[set][3] : nullptr}};
+    tpmg::launch_pack_faces(ctx->launch(), L.nx, L.ny, nz, u, dst);
     CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
     ipc_barrier(ctx);
   } else if (h->loopback) {  // this rank is its own neighbour on every side
-    CUDA_CHECK(cudaMemcpyAsync(rE, sW, nwe * 8, cudaMemcpyDeviceToDevice, ctx->stream));
-    CUDA_CHECK(cudaMemcpyAsync(rW, sE, nwe * 8, cudaMemcpyDeviceToDevice, ctx->stream));
-    CUDA_CHECK(cudaMemcpyAsync(rN, sS, nsn * 8, cudaMemcpyDeviceToDevice, ctx->stream));
-    CUDA_CHECK(cudaMemcpyAsync(rS, sN, nsn * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+    tpmg::launch_pack_faces(ctx->launch(), L.nx, L.ny, nz, u, tpmg::FaceDst{{rE, rW, rN, rS}});
   } else {
+  tpmg::launch_pack_faces(ctx->launch(), L.nx, L.ny, nz, u,
+                          tpmg::FaceDst{{ctx->px > 1 ? sW : nullptr, ctx->px > 1 ? sE : nullptr,
+                                         ctx->py > 1 ? sS : nullptr, ctx->py > 1 ? sN : nullptr}});
   NCCL_CHECK(g_nccl.GroupStart());
   if (ctx->px > 1) {
     const int west = ctx->rank_of(ctx->rx - 1, ctx->ry), east = ctx->rank_of(ctx->rx + 1, ctx->ry);
@@ -478,6 +480,75 @@ Halo exchange(tpmg_hierarchy h, int l, const double* u, int set = 0) {
   if (ys) {
     H.p[2] = rS; H.sk[2] = L.nx; H.st[2] = 1;
     H.p[3] = rN; H.sk[3] = L.nx; H.st[3] = 1;
+  }
+  return H;
+}
+
+// ---- two-cell halo with corners (tpmg::Halo2) ---------------------------------------------
+// Piece d of the deep exchange (d = W, E, S, N, SW, SE, NW, NE) goes to the neighbour in
+// direction d and lands in its Halo2 slot kOpp[d]; offsets of the slots in a recv3 buffer.
+constexpr int kDeepDx[8] = {-1, 1, 0, 0, -1, 1, -1, 1};
+constexpr int kDeepDy[8] = {0, 0, -1, 1, -1, -1, 1, 1};
+constexpr int kOpp[8] = {1, 0, 3, 2, 7, 6, 5, 4};
+int64_t deep_size(const Level& L, int nz) {
+  return (4 * (int64_t)L.ny + 4 * (int64_t)L.nx + 16) * nz;
+}
+void deep_offsets(const Level& L, int nz, int64_t off[8], int64_t cnt[8]) {
+  const int64_t we = 2 * (int64_t)L.ny * nz, sn = 2 * (int64_t)L.nx * nz, c = 4 * (int64_t)nz;
+  const int64_t o[8] = {0, we, 2 * we, 2 * we + sn, 2 * we + 2 * sn, 2 * we + 2 * sn + c,
+                        2 * we + 2 * sn + 2 * c, 2 * we + 2 * sn + 3 * c};
+  const int64_t n[8] = {we, we, sn, sn, c, c, c, c};
+  for (int d = 0; d < 8; ++d) { off[d] = o[d]; cnt[d] = n[d]; }
+}
+// piece d is exchanged when its direction crosses a dimension with several ranks (loopback:
+// every dimension); corners need both
+bool deep_live(tpmg_hierarchy h, int d) {
+  const bool xs = h->ctx->px > 1 || h->loopback, ys = h->ctx->py > 1 || h->loopback;
+  return (kDeepDx[d] == 0 || xs) && (kDeepDy[d] == 0 || ys);
+}
+
+// Exchange u's two-cell faces and 2x2 corners on level l (the fused residual + transpose
+// restriction of a decomposed run reads u two cells beyond its tile) and return the view.
+tpmg::Halo2 exchange_deep(tpmg_hierarchy h, int l, const double* u) {
+  tpmg_context ctx = h->ctx;
+  Level& L = h->lv[l];
+  tpmg::Halo2 H{};
+  H.xs = h->multi() && (ctx->px > 1 || h->loopback);
+  H.ys = h->multi() && (ctx->py > 1 || h->loopback);
+  if (!h->multi()) return H;
+  const int nz = h->nz;
+  int64_t off[8], cnt[8];
+  deep_offsets(L, nz, off, cnt);
+  for (int d = 0; d < 8; ++d) H.p[d] = L.recv3.p + off[d];
+  tpmg::DeepDst dst{};
+  if (ctx->ipc) {
+    CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    ipc_barrier(ctx);
+    for (int d = 0; d < 8; ++d) dst.p[d] = deep_live(h, d) ? L.peer3[d] : nullptr;
+    tpmg::launch_pack_deep(ctx->launch(), L.nx, L.ny, nz, u, dst);
+    CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    ipc_barrier(ctx);
+  } else if (h->loopback) {  // every neighbour is this rank: piece d lands in slot kOpp[d]
+    for (int d = 0; d < 8; ++d) dst.p[d] = L.recv3.p + off[kOpp[d]];
+    tpmg::launch_pack_deep(ctx->launch(), L.nx, L.ny, nz, u, dst);
+  } else {
+    for (int d = 0; d < 8; ++d) dst.p[d] = deep_live(h, d) ? L.send3.p + off[d] : nullptr;
+    tpmg::launch_pack_deep(ctx->launch(), L.nx, L.ny, nz, u, dst);
+    // every rank sends in the order d = 0..7 and receives slot kOpp[d] from the neighbour in
+    // direction kOpp[d] in the same order, so that the pieces two ranks exchange in several
+    // directions (px or py = 2) are matched in order
+    NCCL_CHECK(g_nccl.GroupStart());
+    for (int d = 0; d < 8; ++d) {
+      if (!deep_live(h, d)) continue;
+      NCCL_CHECK(g_nccl.Send(L.send3.p + off[d], cnt[d], ncclDouble,
+                             ctx->rank_of(ctx->rx + kDeepDx[d], ctx->ry + kDeepDy[d]), ctx->comm,
+                             ctx->stream));
+      const int o = kOpp[d];
+      NCCL_CHECK(g_nccl.Recv(L.recv3.p + off[o], cnt[o], ncclDouble,
+                             ctx->rank_of(ctx->rx + kDeepDx[o], ctx->ry + kDeepDy[o]), ctx->comm,
+                             ctx->stream));
+    }
+    NCCL_CHECK(g_nccl.GroupEnd());
   }
   return H;
 }
@@ -638,10 +709,15 @@ void resid_restrict(tpmg_hierarchy h, int lf, const double* u, const double* f, 
     const Halo H = exchange(h, lf, u);
     tpmg::launch_resid_restrict_sum(h->ctx->launch(), h->vcoef(), F.coef(h->nz), h->xi, u, H, f,
                                     coarse);
-  } else if (!h->multi() && h->fuse_rr && tpmg::resid_restrict_T_fusable(F.coef(h->nz))) {
+  } else if (h->fuse_rr && tpmg::resid_restrict_T_fusable(F.coef(h->nz)) &&
+             (!h->multi() || (F.d_ringc.p && tpmg::resid_restrict_T2_fusable(F.coef(h->nz))))) {
+    // decomposed: u's two-cell halo with corners and f's face halo first (the ring residuals
+    // the transpose stencil reaches outside the tile)
+    const tpmg::Halo2 hu = exchange_deep(h, lf, u);
+    const Halo hf = exchange(h, lf, f, 0);
     if (probe) probe_begin(h, TPMG_K_RESID_RESTRICT);
-    tpmg::launch_resid_restrict_T(h->ctx->launch(), h->vcoef(), F.coef(h->nz), h->xi, u, f,
-                                  coarse);
+    tpmg::launch_resid_restrict_T(h->ctx->launch(), h->vcoef(), F.coef(h->nz), h->xi, u, hu, f,
+                                  hf, F.d_ringc.p, coarse);
     if (probe) probe_end(h, TPMG_K_RESID_RESTRICT);
   } else {
     apply_level(h, lf, tpmg::APPLY_RESID, u, f, scratch);
@@ -1157,14 +1233,14 @@ void ipc_connect(tpmg_hierarchy h) {
   const int nl = (int)h->lv.size();
   if (nl > kIpcMaxLevels) throw Error(TPMG_E_CONFIG, "ipc transport: too many levels");
   for (int l = 0; l < nl; ++l)
-    for (int set = 0; set < 2; ++set) {
-      const double* b = set ? h->lv[l].recv2.p : h->lv[l].recv.p;
+    for (int set = 0; set < 3; ++set) {
+      const double* b = set == 2 ? h->lv[l].recv3.p : (set ? h->lv[l].recv2.p : h->lv[l].recv.p);
       if (b) CUDA_CHECK(cudaIpcGetMemHandle(&S->handles[ctx->rank][l][set], (void*)b));
     }
   ipc_barrier(ctx);
   std::unordered_map<int64_t, double*> opened;
   auto base = [&](int r, int l, int set) {
-    const int64_t key = ((int64_t)r * kIpcMaxLevels + l) * 2 + set;
+    const int64_t key = ((int64_t)r * kIpcMaxLevels + l) * 3 + set;
     auto it = opened.find(key);
     if (it != opened.end()) return it->second;
     void* p = nullptr;
@@ -1187,6 +1263,14 @@ void ipc_connect(tpmg_hierarchy h) {
         L.peer[set][2] = base(south, l, set) + 2 * nwe + nsn;  // -> south's N segment
         L.peer[set][3] = base(north, l, set) + 2 * nwe;        // -> north's S segment
       }
+    }
+    if (L.recv3.p) {  // deep piece d -> slot kOpp[d] of the neighbour in direction d
+      int64_t off[8], cnt[8];
+      deep_offsets(L, h->nz, off, cnt);
+      for (int d = 0; d < 8; ++d)
+        if (deep_live(h, d))
+          L.peer3[d] = base(ctx->rank_of(ctx->rx + kDeepDx[d], ctx->ry + kDeepDy[d]), l, 2) +
+                       off[kOpp[d]];
     }
   }
   ipc_barrier(ctx);
@@ -1347,6 +1431,35 @@ int hier_create_impl(tpmg_context ctx, const tpmg_grid_desc* g, const tpmg_facto
       L.d_ss.upload(ss.data(), L.plane);
       L.d_sn.upload(sn.data(), L.plane);
       L.cm = cm;
+      if (h->multi() && cm == tpmg::CM_FACT && l > 0) {
+        // the same scalars on the 1-cell ring around the tile (tpmg::kRingFields layout), for the
+        // ring residuals of the decomposed fused residual + transpose restriction
+        const int64_t rn = 2 * (int64_t)L.ny + 2 * (int64_t)L.nx;
+        std::vector<double> rc(tpmg::kRingFields * rn);
+        auto put = [&](int64_t ri, int64_t gi, int64_t gj) {
+          gi = (gi % gx + gx) % gx;
+          gj = (gj % gy + gy) % gy;
+          const int64_t G = gj * gx + gi;
+          const int64_t gw = gj * gx + (gi + gx - 1) % gx;
+          const int64_t gs = ((gj + gy - 1) % gy) * gx + gi;
+          rc[ri] = area * pb[G];
+          rc[rn + ri] = w2 * (area * pa[G]);
+          rc[2 * rn + ri] = w2 * (area * px[G]);
+          rc[3 * rn + ri] = w2 * ge_e * ps[gw];
+          rc[4 * rn + ri] = w2 * ge_e * ps[G];
+          rc[5 * rn + ri] = w2 * ge_n * ps[gnc + gs];
+          rc[6 * rn + ri] = w2 * ge_n * ps[gnc + G];
+        };
+        for (int j = 0; j < L.ny; ++j) {
+          put(j, L.x0 - 1, L.y0 + j);
+          put(L.ny + j, L.x0 + L.nx, L.y0 + j);
+        }
+        for (int i = 0; i < L.nx; ++i) {
+          put(2 * L.ny + i, L.x0 + i, L.y0 - 1);
+          put(2 * L.ny + L.nx + i, L.x0 + i, L.y0 + L.ny);
+        }
+        L.d_ringc.upload(rc.data(), rc.size());
+      }
       if (cm != tpmg::CM_FACT) {
         // assemble_hatted, dense components (discretization.hpp:122-140, 196-203):
         // alpha_r hat = ((w2 |T|) f_k) alpha_r; beta hat = |T| (dz_k beta);
@@ -1473,6 +1586,13 @@ int hier_create_impl(tpmg_context ctx, const tpmg_grid_desc* g, const tpmg_facto
         const int64_t faces = 2 * (int64_t)L.ny * nz + 2 * (int64_t)L.nx * nz;
         L.send.alloc(faces);
         L.recv.alloc(faces);
+        // two-cell halo of the decomposed fused residual + transpose restriction
+        if (L.d_ringc.p && tpmg::resid_restrict_T2_fusable(L.coef(nz))) {
+          L.send3.alloc(deep_size(L, nz));
+          L.recv3.alloc(deep_size(L, nz));
+        } else {
+          L.d_ringc.reset();
+        }
       }
       // one partial per 256-column block (k_apply) or per 32x4 tile (k_apply_tiled)
       max_blocks = std::max<int64_t>(max_blocks, (L.plane + 255) / 256 + 1);

@@ -80,6 +80,31 @@ struct Halo {
   int64_t st[4];
 };
 
+// Two-cell halo with corners (the fused residual + transpose restriction of a decomposed run
+// reads u two cells beyond its tile).  Receive buffers, per level k:
+//   p[0] W2 [k][j][c] = u(-2+c, j)     p[1] E2 [k][j][c] = u(nx+c, j)      (2*ny per level)
+//   p[2] S2 [k][r][i] = u(i, -2+r)     p[3] N2 [k][r][i] = u(i, ny+r)      (2*nx per level)
+//   p[4..7] corners SW, SE, NW, NE [k][r][c] = u(-2+c | nx+c, -2+r | ny+r)  (4 per level)
+// xs / ys: 0 = that dimension has one rank (periodic wrap onto the tile itself, no buffers).
+struct Halo2 {
+  const double* p[8];
+  int xs, ys;
+};
+// Where each packed halo piece lands (send buffer, a neighbour's receive buffer through a CUDA-IPC
+// mapping, or this rank's own receive buffer in loopback); nullptr: the piece is not exchanged.
+// Faces: W, E, S, N (1-cell, [k][j] / [k][i]).  Deep pieces: W, E, S, N, SW, SE, NW, NE in the
+// Halo2 layouts of the receiving side (piece W = columns 0..1 -> the west rank's E2, ...).
+struct FaceDst {
+  double* p[4];
+};
+struct DeepDst {
+  double* p[8];
+};
+// Ring of 1-cell coefficient scalars around the local tile (a decomposed run's fused residual +
+// restriction forms residuals on it): 7 arrays (bh, ah, xh, sw, se, ss, sn) of 2*ny + 2*nx
+// entries each, ring index W j, E ny+j, S 2ny+i, N 2ny+nx+i.
+constexpr int kRingFields = 7;
+
 enum ApplyMode { APPLY_AU = 0, APPLY_RESID = 1 };
 
 // Deterministic reduction workspace: per-block partials, then one fixed-order pass.
@@ -191,10 +216,15 @@ void launch_restrict_sum(const Launch& L, int cnx, int cny, int nz, const double
 // coarse = R_sum(f - A u) fused (multigrid.hpp:285-291), u on the fine level.
 void launch_resid_restrict_sum(const Launch& L, const VertCoef& V, const LevelCoef& Cf, bool xi,
                                const double* u, const Halo& H, const double* f, double* coarse);
-// coarse = P^T (f - A u) fused, single GPU (periodic wrap, 2-cell u halo inside the kernel).
+// coarse = P^T (f - A u) fused.  One rank: periodic wrap inside the kernel (hu.xs = hu.ys = 0,
+// hf = self_halo(f), ringc = nullptr).  Decomposed (resid_restrict_T2_fusable levels, factorised
+// coefficients): u's two-cell halo with corners in hu, f's face halo in hf, the coefficient ring
+// in ringc.
 bool resid_restrict_T_fusable(const LevelCoef& Cf);
+bool resid_restrict_T2_fusable(const LevelCoef& Cf);
 void launch_resid_restrict_T(const Launch& L, const VertCoef& V, const LevelCoef& Cf, bool xi,
-                             const double* u, const double* f, double* coarse);
+                             const double* u, const Halo2& hu, const double* f, const Halo& hf,
+                             const double* ringc, double* coarse);
 // coarse = P^T fine (restrict_field_transpose, multigrid.hpp:46-69); Hf: fine face halo.
 void launch_restrict_transpose(const Launch& L, int cnx, int cny, int nz, const double* fine,
                                const Halo& Hf, double* coarse);
@@ -230,7 +260,9 @@ void launch_xfast_to_kfast(const Launch& L, int64_t ncol, int nz, const double* 
 void launch_fill(const Launch& L, int64_t n, double* p, double v);
 void launch_fill_hash(const Launch& L, int64_t n, double* p, double v, uint64_t seed);
 
-// Multi-GPU halo packing: face values of u into send buffers [W|E|S|N] of sizes ny*nz,ny*nz,nx*nz,nx*nz.
-void launch_pack_faces(const Launch& L, int nx, int ny, int nz, const double* u, double* send);
+// Multi-GPU halo packing: the face values of u ([k][j] W/E, [k][i] S/N) written to dst.
+void launch_pack_faces(const Launch& L, int nx, int ny, int nz, const double* u, const FaceDst& dst);
+// The two-cell faces and 2x2 corners of u (Halo2 layouts of the receiving ranks) written to dst.
+void launch_pack_deep(const Launch& L, int nx, int ny, int nz, const double* u, const DeepDst& dst);
 
 }  // namespace tpmg

@@ -20,6 +20,11 @@ PROBLEMS = {
     "tiled": lambda: synth.make_problem(128, 64, 16, omega2=1e-2, lambda2=1e-4,
                                         grading="quadratic", profile="uniform", profile_seed=3,
                                         depth=4, name="tiled"),
+    # every rank's finest tile above the coarse regime (> 4096 columns): the decomposed fused
+    # residual + transpose restriction with its two-cell halo, corners and coefficient ring
+    "rr2": lambda: synth.make_problem(256, 128, 16, omega2=1e-2, lambda2=1e-4,
+                                      grading="geometric", ratio=1.2, profile="lognormal",
+                                      profile_seed=6, profile_sigma=0.5, depth=4, name="rr2"),
     "cfg5s": lambda: synth.make_problem(64, 64, 16, omega2=1e-5, lambda2=1e-6,
                                         grading="geometric", ratio=1.1, profile="lognormal",
                                         profile_seed=2, depth=4, nu=2, tol=1e-10, name="cfg5-small"),
