@@ -142,3 +142,101 @@ def test_tiles_and_halo_protocol_reproduce_global_apply(px, py):
         assert dot_err <= 1e-13
         tiles.add(t)
     assert len(tiles) == world  # disjoint tiles
+
+
+# ---- the two-cell halo with corners (tpmg_host.cpp:exchange_deep, tpmg::Halo2) ----------------
+DDX = (-1, 1, 0, 0, -1, 1, -1, 1)   # pieces W, E, S, N, SW, SE, NW, NE (kDeepDx / kDeepDy)
+DDY = (0, 0, -1, 1, -1, -1, 1, 1)
+OPP = (1, 0, 3, 2, 7, 6, 5, 4)       # kOpp: piece d lands in the receiver's slot OPP[d]
+
+
+def _deep_pieces(u):
+    """k_pack_deep's pieces: W/E [k][j][c] from columns c / nx-2+c, S/N [k][r][i] from rows
+    r / ny-2+r, corners [k][r][c] from the 2x2 corner blocks."""
+    return [np.ascontiguousarray(a) for a in (
+        u[:, :, 0:2], u[:, :, -2:], u[:, 0:2, :], u[:, -2:, :],
+        u[:, 0:2, 0:2], u[:, 0:2, -2:], u[:, -2:, 0:2], u[:, -2:, -2:])]
+
+
+def _halo2_window(u, slots, xs, ys):
+    """The (nz, ny+4, nx+4) block halo2_at reads: inside from u, outside from the slots
+    (W2, E2, S2, N2, SW, SE, NW, NE), a dimension with one rank wrapping onto the tile."""
+    nz, ny, nx = u.shape
+    out = np.empty((nz, ny + 4, nx + 4))
+    for gy in range(-2, ny + 2):
+        for gx in range(-2, nx + 2):
+            x, y = gx, gy
+            if not xs:
+                x %= nx
+            if not ys:
+                y %= ny
+            ox = -1 if x < 0 else (1 if x >= nx else 0)
+            oy = -1 if y < 0 else (1 if y >= ny else 0)
+            c = x + 2 if ox < 0 else x - nx
+            r = y + 2 if oy < 0 else y - ny
+            if ox == 0 and oy == 0:
+                v = u[:, y, x]
+            elif oy == 0:
+                v = slots[0 if ox < 0 else 1][:, y, c]
+            elif ox == 0:
+                v = slots[2 if oy < 0 else 3][:, r, x]
+            else:
+                v = slots[4 + (0 if oy < 0 else 2) + (0 if ox < 0 else 1)][:, r, c]
+            out[:, gy + 2, gx + 2] = v
+    return out
+
+
+def _deep_worker(rank, world, px, py, port, q):
+    import torch
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        NX, NY, NZ = 16 * px, 8 * py, 3
+        tnx, tny = NX // px, NY // py
+        rx, ry = rank % px, rank // px
+        x0, y0 = rx * tnx, ry * tny
+        u_glob = np.random.default_rng(11).standard_normal((NZ, NY, NX))
+        u = np.ascontiguousarray(u_glob[:, y0:y0 + tny, x0:x0 + tnx])
+        xs, ys = px > 1, py > 1
+        live = [(DDX[d] == 0 or xs) and (DDY[d] == 0 or ys) for d in range(8)]
+        nbr = [((ry + DDY[d]) % py) * px + (rx + DDX[d]) % px for d in range(8)]
+        pieces = _deep_pieces(u)
+        slots = [np.zeros_like(p) for p in (pieces[1], pieces[0], pieces[3], pieces[2],
+                                            pieces[7], pieces[6], pieces[5], pieces[4])]
+        recv = [torch.from_numpy(s) for s in slots]
+        ops = []
+        for d in range(8):  # exchange_deep's NCCL group: send d, receive slot OPP[d]
+            if not live[d]:
+                continue
+            ops.append(dist.P2POp(dist.isend, torch.from_numpy(pieces[d]), nbr[d]))
+            ops.append(dist.P2POp(dist.irecv, recv[OPP[d]], nbr[OPP[d]]))
+        for w in dist.batch_isend_irecv(ops) if ops else []:
+            w.wait()
+        win = _halo2_window(u, [r.numpy() for r in recv], xs, ys)
+        ref = np.take(np.take(u_glob, np.arange(y0 - 2, y0 + tny + 2) % NY, axis=1),
+                      np.arange(x0 - 2, x0 + tnx + 2) % NX, axis=2)
+        q.put((rank, bool(np.array_equal(win, ref))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("px,py", [(2, 1), (1, 2), (2, 2), (4, 2)])
+def test_deep_halo_protocol_reproduces_the_periodic_window(px, py):
+    """The decomposed fused residual + restriction's exchange (8 pieces, sends in the order
+    W,E,S,N,SW,SE,NW,NE, receives into the opposite slots in the same order, so that pieces two
+    ranks exchange in several directions -- px or py = 2, where W = E and all diagonals coincide
+    -- match like an NCCL group) gives every tile the global field two cells beyond it."""
+    world = px * py
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_deep_worker, args=(r, world, px, py, port, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok in res), res
