@@ -65,6 +65,8 @@ struct Nccl {
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  // optional (NCCL >= 2.18): the second communicator of the side-stream halo exchanges
+  ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*) = nullptr;
 
   void load() {
     if (handle) return;
@@ -87,6 +89,7 @@ struct Nccl {
     AllReduce = (decltype(AllReduce))sym("ncclAllReduce");
     AllGather = (decltype(AllGather))sym("ncclAllGather");
     GetErrorString = (decltype(GetErrorString))sym("ncclGetErrorString");
+    CommSplit = (decltype(CommSplit))dlsym(handle, "ncclCommSplit");
   }
 };
 Nccl g_nccl;
@@ -126,6 +129,11 @@ struct tpmg_context_s {
   int rank = 0, world = 1, px = 1, py = 1, rx = 0, ry = 0;
   cudaStream_t stream = nullptr;
   ncclComm_t comm = nullptr;
+  // side stream of the halo exchanges that overlap compute (exchange_f_async), with its own
+  // communicator so that its NCCL operations never interleave with the main stream's
+  cudaStream_t side = nullptr;
+  ncclComm_t comm2 = nullptr;
+  tpmg::Launch side_launch() { return tpmg::Launch{side, &launches}; }
   // CUDA-IPC transport (tpmg_init_ipc): shared segment, reduction phase, pinned staging
   IpcShm* ipc = nullptr;
   int ipc_phase = 0;
@@ -186,6 +194,8 @@ struct Level {
   DevBuf send2, recv2;         // finest level: a second set (z and p_old before the fused A p)
   DevBuf send3, recv3;         // two-cell halo with corners (tpmg::Halo2 layout, fused R(f - A u))
   DevBuf d_ringc;              // coefficient scalars on the 1-cell ring around the tile
+  DevBuf sendF, recvF;         // face halo of f posted early on the side stream (exchange_f_async)
+  bool f_pending = false;      // recvF is being filled for this level's next residual + restriction
   // IPC transport: where this rank's W / E / S / N faces land in the neighbours' receive
   // buffers (per halo set), and its deep pieces W, E, S, N, SW, SE, NW, NE
   double* peer[2][4] = {{nullptr, nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr, nullptr}};
@@ -271,6 +281,11 @@ struct tpmg_hierarchy_s {
   uint32_t probe_pending = 0;  // pairs recorded by the work queued since the last collection
   std::unordered_map<const void*, uint32_t> iter_graph_probes;
   std::vector<void*> ipc_mapped;  // neighbours' receive buffers opened through CUDA IPC
+  // exchange_f_async: per level, f ready on the main stream / halo landed on the side stream
+  std::vector<cudaEvent_t> ev_fsrc, ev_fdone;
+  // which direction buffer's face halo set 1 (recv2) holds: the fused A p pass of a decomposed
+  // run exchanges p_new once and both the r-update sweep and the next A p pass read it
+  const double* p_halo_of = nullptr;
   int finest() const { return (int)lv.size() - 1; }
   VertCoef vcoef() const {
     VertCoef v{d_bv.p, d_sv.p, d_av.p, d_xv.p};
@@ -294,6 +309,8 @@ struct tpmg_hierarchy_s {
     d_vx.upload(vx.data(), vx.size());
   }
   ~tpmg_hierarchy_s() {
+    for (cudaEvent_t e : ev_fsrc) cudaEventDestroy(e);
+    for (cudaEvent_t e : ev_fdone) cudaEventDestroy(e);
     for (auto& pr : probes) {
       if (pr.e0) cudaEventDestroy(pr.e0);
       if (pr.e1) cudaEventDestroy(pr.e1);
@@ -419,14 +436,33 @@ int plan_levels(int64_t NX, int64_t NY, int px, int py, int depth, bool linear) 
 // Exchange the 1-cell faces of u on level l with the 4 neighbouring ranks and return the
 // view the kernels read across the tile faces.  Dimensions with a single rank wrap onto the
 // tile itself (periodic) without any copy.
+// The view of halo set `set` of level l as exchange() leaves it (receive buffers across the
+// dimensions with several ranks, the periodic self views across the others).
+Halo halo_view(tpmg_hierarchy h, int l, const double* u, int set) {
+  tpmg_context ctx = h->ctx;
+  Level& L = h->lv[l];
+  Halo H = tpmg::self_halo(u, L.nx, L.ny, L.plane);
+  if (!h->multi()) return H;
+  const bool xs = ctx->px > 1 || h->loopback, ys = ctx->py > 1 || h->loopback;
+  const int64_t nwe = (int64_t)L.ny * h->nz, nsn = (int64_t)L.nx * h->nz;
+  double* rW = (set ? L.recv2 : L.recv).p;
+  if (xs) {
+    H.p[0] = rW; H.sk[0] = L.ny; H.st[0] = 1;
+    H.p[1] = rW + nwe; H.sk[1] = L.ny; H.st[1] = 1;
+  }
+  if (ys) {
+    H.p[2] = rW + 2 * nwe; H.sk[2] = L.nx; H.st[2] = 1;
+    H.p[3] = rW + 2 * nwe + nsn; H.sk[3] = L.nx; H.st[3] = 1;
+  }
+  return H;
+}
+
 Halo exchange(tpmg_hierarchy h, int l, const double* u, int set = 0) {
   tpmg_context ctx = h->ctx;
   Level& L = h->lv[l];
   DevBuf& SB = set ? L.send2 : L.send;
   DevBuf& RB = set ? L.recv2 : L.recv;
-  Halo H = tpmg::self_halo(u, L.nx, L.ny, L.plane);
-  if (!h->multi()) return H;
-  const bool xs = ctx->px > 1 || h->loopback, ys = ctx->py > 1 || h->loopback;
+  if (!h->multi()) return tpmg::self_halo(u, L.nx, L.ny, L.plane);
   const int nz = h->nz;
   const int64_t nwe = (int64_t)L.ny * nz, nsn = (int64_t)L.nx * nz;
   double* sW = SB.p;
@@ -473,15 +509,7 @@ Halo exchange(tpmg_hierarchy h, int l, const double* u, int set = 0) {
   }
   NCCL_CHECK(g_nccl.GroupEnd());
   }
-  if (xs) {
-    H.p[0] = rW; H.sk[0] = L.ny; H.st[0] = 1;
-    H.p[1] = rE; H.sk[1] = L.ny; H.st[1] = 1;
-  }
-  if (ys) {
-    H.p[2] = rS; H.sk[2] = L.nx; H.st[2] = 1;
-    H.p[3] = rN; H.sk[3] = L.nx; H.st[3] = 1;
-  }
-  return H;
+  return halo_view(h, l, u, set);
 }
 
 // ---- two-cell halo with corners (tpmg::Halo2) ---------------------------------------------
@@ -549,6 +577,91 @@ tpmg::Halo2 exchange_deep(tpmg_hierarchy h, int l, const double* u) {
                              ctx->stream));
     }
     NCCL_CHECK(g_nccl.GroupEnd());
+  }
+  return H;
+}
+
+// ---- halo exchanges that overlap compute ---------------------------------------------------
+// A coarse level's right-hand side f_l is formed by the residual + restriction of level l+1
+// and its face halo is next needed by level l's own residual + restriction, after its
+// pre-sweeps (which read f_l only in their own columns).  The exchange is therefore posted on
+// the side stream right away (its own buffers, its own NCCL communicator) and overlaps those
+// sweeps; the main stream waits for it only at the residual + restriction.  Loopback and NCCL
+// runs; the CUDA-IPC transport orders its exchanges by host barriers and keeps them in place.
+bool f_async_ok(tpmg_hierarchy h) {
+  tpmg_context ctx = h->ctx;
+  if (!h->multi() || ctx->ipc || !ctx->side) return false;
+  return h->loopback || ctx->comm2;
+}
+
+void exchange_f_async(tpmg_hierarchy h, int l, const double* f) {
+  tpmg_context ctx = h->ctx;
+  Level& L = h->lv[l];
+  if (!f_async_ok(h) || !L.recvF.p) return;
+  if (h->ev_fsrc.empty()) {
+    h->ev_fsrc.assign(h->lv.size(), nullptr);
+    h->ev_fdone.assign(h->lv.size(), nullptr);
+    for (size_t i = 0; i < h->lv.size(); ++i) {
+      CUDA_CHECK(cudaEventCreateWithFlags(&h->ev_fsrc[i], cudaEventDisableTiming));
+      CUDA_CHECK(cudaEventCreateWithFlags(&h->ev_fdone[i], cudaEventDisableTiming));
+    }
+  }
+  const int nz = h->nz;
+  const int64_t nwe = (int64_t)L.ny * nz, nsn = (int64_t)L.nx * nz;
+  double* sW = L.sendF.p;
+  double* sE = sW + nwe;
+  double* sS = sE + nwe;
+  double* sN = sS + nsn;
+  double* rW = L.recvF.p;
+  double* rE = rW + nwe;
+  double* rS = rE + nwe;
+  double* rN = rS + nsn;
+  CUDA_CHECK(cudaEventRecord(h->ev_fsrc[l], ctx->stream));
+  CUDA_CHECK(cudaStreamWaitEvent(ctx->side, h->ev_fsrc[l], 0));
+  if (h->loopback) {
+    tpmg::launch_pack_faces(ctx->side_launch(), L.nx, L.ny, nz, f, tpmg::FaceDst{{rE, rW, rN, rS}});
+  } else {
+    tpmg::launch_pack_faces(ctx->side_launch(), L.nx, L.ny, nz, f,
+                            tpmg::FaceDst{{ctx->px > 1 ? sW : nullptr, ctx->px > 1 ? sE : nullptr,
+                                           ctx->py > 1 ? sS : nullptr, ctx->py > 1 ? sN : nullptr}});
+    NCCL_CHECK(g_nccl.GroupStart());
+    if (ctx->px > 1) {
+      const int west = ctx->rank_of(ctx->rx - 1, ctx->ry), east = ctx->rank_of(ctx->rx + 1, ctx->ry);
+      NCCL_CHECK(g_nccl.Send(sW, nwe, ncclDouble, west, ctx->comm2, ctx->side));
+      NCCL_CHECK(g_nccl.Send(sE, nwe, ncclDouble, east, ctx->comm2, ctx->side));
+      NCCL_CHECK(g_nccl.Recv(rE, nwe, ncclDouble, east, ctx->comm2, ctx->side));
+      NCCL_CHECK(g_nccl.Recv(rW, nwe, ncclDouble, west, ctx->comm2, ctx->side));
+    }
+    if (ctx->py > 1) {
+      const int south = ctx->rank_of(ctx->rx, ctx->ry - 1), north = ctx->rank_of(ctx->rx, ctx->ry + 1);
+      NCCL_CHECK(g_nccl.Send(sS, nsn, ncclDouble, south, ctx->comm2, ctx->side));
+      NCCL_CHECK(g_nccl.Send(sN, nsn, ncclDouble, north, ctx->comm2, ctx->side));
+      NCCL_CHECK(g_nccl.Recv(rN, nsn, ncclDouble, north, ctx->comm2, ctx->side));
+      NCCL_CHECK(g_nccl.Recv(rS, nsn, ncclDouble, south, ctx->comm2, ctx->side));
+    }
+    NCCL_CHECK(g_nccl.GroupEnd());
+  }
+  CUDA_CHECK(cudaEventRecord(h->ev_fdone[l], ctx->side));
+  L.f_pending = true;
+}
+
+// the main stream waits for level l's posted f halo; returns its view (exchange()'s layout)
+Halo finish_f_async(tpmg_hierarchy h, int l, const double* f) {
+  tpmg_context ctx = h->ctx;
+  Level& L = h->lv[l];
+  CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, h->ev_fdone[l], 0));
+  L.f_pending = false;
+  Halo H = tpmg::self_halo(f, L.nx, L.ny, L.plane);
+  const bool xs = ctx->px > 1 || h->loopback, ys = ctx->py > 1 || h->loopback;
+  const int64_t nwe = (int64_t)L.ny * h->nz, nsn = (int64_t)L.nx * h->nz;
+  double* rW = L.recvF.p;
+  if (xs) {
+    H.p[0] = rW; H.sk[0] = L.ny; H.st[0] = 1;
+    H.p[1] = rW + nwe; H.sk[1] = L.ny; H.st[1] = 1;
+  }
+  if (ys) {
+    H.p[2] = rW + 2 * nwe; H.sk[2] = L.nx; H.st[2] = 1;
+    H.p[3] = rW + 2 * nwe + nsn; H.sk[3] = L.nx; H.st[3] = 1;
   }
   return H;
 }
@@ -667,9 +780,9 @@ void dot_into(tpmg_hierarchy h, int l, const double* a, const double* b, int slo
 
 // ---- hot-path building blocks ------------------------------------------------------------
 void apply_level(tpmg_hierarchy h, int l, int mode, const double* u, const double* f, double* y,
-                 int dot_slot = -1) {
+                 int dot_slot = -1, int set = 0) {
   Level& L = h->lv[l];
-  const Halo H = exchange(h, l, u);
+  const Halo H = exchange(h, l, u, set);
   int nb = 0;
   tpmg::launch_apply(h->ctx->launch(), h->vcoef(), L.coef(h->nz), h->xi, mode, u, H, f, y,
                      dot_slot >= 0 ? h->partials.p : nullptr, &nb);
@@ -680,11 +793,13 @@ void apply_level(tpmg_hierarchy h, int l, int mode, const double* u, const doubl
 // per-tile partials are reduced into scalar slot `slot`.
 void sweep(tpmg_hierarchy h, int l, const double* u_in, const double* f, double* out,
            const tpmg::PcgFuse* fz = nullptr, int slot = -1, const tpmg::ProSrc* pro = nullptr,
-           int probe = -1) {
+           int probe = -1, const Halo* p_halo = nullptr) {
   Level& L = h->lv[l];
-  // the haloed input: u, or p when the zero-guess sweep forms q = A p itself
+  // the haloed input: u, or p when the zero-guess sweep forms q = A p itself (p_halo: p's halo
+  // already exchanged by the caller)
   Halo H = u_in ? exchange(h, l, u_in)
-                : (fz && fz->p ? exchange(h, l, fz->p) : tpmg::self_halo(out, L.nx, L.ny, L.plane));
+                : (fz && fz->p ? (p_halo ? *p_halo : exchange(h, l, fz->p))
+                               : tpmg::self_halo(out, L.nx, L.ny, L.plane));
   int nb = 0;
   if (probe >= 0) probe_begin(h, probe);
   tpmg::launch_jacobi(h->ctx->launch(), h->vcoef(), L.coef(h->nz), h->xi, u_in, H, f, out,
@@ -700,6 +815,9 @@ void resid_restrict(tpmg_hierarchy h, int lf, const double* u, const double* f, 
                     double* scratch, bool probe = false) {
   Level& F = h->lv[lf];
   Level& C = h->lv[lf - 1];
+  // f's face halo posted early by exchange_f_async (joined here whichever path runs)
+  const bool f_posted = F.f_pending;
+  const Halo hf_posted = f_posted ? finish_f_async(h, lf, f) : Halo{};
   if (h->generic) {
     apply_level(h, lf, tpmg::APPLY_RESID, u, f, scratch);
     restrict_plain(h, lf, scratch, coarse, -1);
@@ -714,7 +832,7 @@ void resid_restrict(tpmg_hierarchy h, int lf, const double* u, const double* f, 
     // decomposed: u's two-cell halo with corners and f's face halo first (the ring residuals
     // the transpose stencil reaches outside the tile)
     const tpmg::Halo2 hu = exchange_deep(h, lf, u);
-    const Halo hf = exchange(h, lf, f, 0);
+    const Halo hf = f_posted ? hf_posted : exchange(h, lf, f, 0);
     if (probe) probe_begin(h, TPMG_K_RESID_RESTRICT);
     tpmg::launch_resid_restrict_T(h->ctx->launch(), h->vcoef(), F.coef(h->nz), h->xi, u, hu, f,
                                   hf, F.d_ringc.p, coarse);
@@ -772,7 +890,7 @@ void fill(tpmg_hierarchy h, double* p, int64_t n, double v) {
 // f_pre and writes the updated r to fz.r == f, so r = f_0 never needs a device copy
 void vcycle(tpmg_hierarchy h, int l, const double* f, double* A, double* B, bool zero,
             bool pcg_fuse = false, const double* p_dir = nullptr,
-            const double* f_pre = nullptr) {
+            const double* f_pre = nullptr, const Halo* p_halo = nullptr) {
   Level& L = h->lv[l];
   const int64_t n = L.plane * h->nz;
   const int npre = h->nu_pre[l], npost = h->nu_post[l], total = npre + npost;
@@ -793,7 +911,7 @@ void vcycle(tpmg_hierarchy h, int l, const double* f, double* A, double* B, bool
       // first sweep from zero writes where the last sweep must end in A
       cur = ((total - 1) % 2 == 0) ? A : B;
       sweep(h, l, nullptr, (pcg_fuse && f_pre) ? f_pre : f, cur, pcg_fuse ? &fz : nullptr, 2,
-            nullptr, pcg_fuse ? TPMG_K_PCG_RUPDATE : -1);
+            nullptr, pcg_fuse ? TPMG_K_PCG_RUPDATE : -1, p_halo);
       s0 = 1;
     } else {
       cur = (npost % 2 == 0) ? A : B;
@@ -811,6 +929,8 @@ void vcycle(tpmg_hierarchy h, int l, const double* f, double* A, double* B, bool
   if (l > 0) {
     Level& C = h->lv[l - 1];
     resid_restrict(h, l, cur, f, C.f.p, other(cur), pcg_fuse);
+    // decomposed: f_{l-1}'s face halo travels while level l-1 pre-smooths
+    if (l - 1 > 0 && C.recvF.p) exchange_f_async(h, l - 1, C.f.p);
     vcycle(h, l - 1, C.f.p, C.u.p, C.t.p, true);
     fuse_pro = npost > 0 && !h->multi() && !h->generic &&
                h->prolongation == TPMG_PROLONG_LINEAR && tpmg::jacobi_prolong_fusable(L.coef(h->nz));
@@ -895,7 +1015,11 @@ void pcg_iteration(tpmg_hierarchy h, double* x, bool first, int pc) {
       double* po = h->pbuf(pc);
       int nb = 0;
       // halos of z and p_old (single rank: the periodic self views, no copy)
-      const Halo Hz = exchange(h, L, h->z.p, 0), Hp = exchange(h, L, po, 1);
+      // p_reuse: p_old's halo is already in set 1 (exchanged once, right after the pass that
+      // formed it, for that iteration's r-update sweep)
+      const bool p_reuse = h->multi() && h->q_in_sweep;
+      const Halo Hz = exchange(h, L, h->z.p, 0);
+      const Halo Hp = p_reuse ? halo_view(h, L, po, 1) : exchange(h, L, po, 1);
       probe_begin(h, TPMG_K_PCG_DIRECTION);
       tpmg::launch_pcg_ap(ctx->launch(), h->vcoef(), F.coef(h->nz), h->xi, h->z.p, Hz, po, Hp,
                           h->pbuf(pc ^ 1),
@@ -903,15 +1027,20 @@ void pcg_iteration(tpmg_hierarchy h, double* x, bool first, int pc) {
       probe_end(h, TPMG_K_PCG_DIRECTION);
       tpmg::launch_copy_scalar(ctx->launch(), h->scal.p, 0, 3);
       finish_dot(h, nb, 1, L);
+      Halo Hpn;
+      if (p_reuse) Hpn = exchange(h, L, h->pbuf(pc ^ 1), 1);
       vcycle(h, L, h->r.p, h->z.p, h->tmp.p, true, true,
-             h->q_in_sweep ? h->pbuf(pc ^ 1) : nullptr);
+             h->q_in_sweep ? h->pbuf(pc ^ 1) : nullptr, nullptr, p_reuse ? &Hpn : nullptr);
       return;
     } else {
       if (!first) {
         tpmg::launch_pcg_px(ctx->launch(), n, h->scal.p, h->z.p, h->pbuf(pc), x);
         tpmg::launch_copy_scalar(ctx->launch(), h->scal.p, 0, 3);
       }
-      apply_level(h, L, tpmg::APPLY_AU, h->pbuf(pc), nullptr, h->q.p, 1);
+      // decomposed fused A p schedule: p's halo goes to set 1, where the next A p pass reads
+      // it as p_old's
+      apply_level(h, L, tpmg::APPLY_AU, h->pbuf(pc), nullptr, h->q.p, 1,
+                  h->multi() && h->q_in_sweep ? 1 : 0);
     }
     vcycle(h, L, h->r.p, h->z.p, h->tmp.p, true, true, nullptr, first ? h->f_first : nullptr);
     return;
@@ -1107,7 +1236,9 @@ int tpmg_init(const tpmg_context_params* prm, tpmg_context* out) {
       ncclUniqueId id;
       std::memcpy(&id, prm->nccl_id, sizeof(id));
       NCCL_CHECK(g_nccl.CommInitRank(&ctx->comm, ctx->world, id, ctx->rank));
+      if (g_nccl.CommSplit) NCCL_CHECK(g_nccl.CommSplit(ctx->comm, 0, ctx->rank, &ctx->comm2, nullptr));
     }
+    CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
     *out = ctx.release();
   });
 }
@@ -1184,7 +1315,9 @@ int tpmg_finalize(tpmg_context ctx) {
   if (!ctx) return TPMG_OK;
   if (ctx->ipc) munmap(ctx->ipc, sizeof(IpcShm));
   if (ctx->ipc_host) cudaFreeHost(ctx->ipc_host);
+  if (ctx->comm2) g_nccl.CommDestroy(ctx->comm2);
   if (ctx->comm) g_nccl.CommDestroy(ctx->comm);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return TPMG_OK;
@@ -1590,6 +1723,10 @@ int hier_create_impl(tpmg_context ctx, const tpmg_grid_desc* g, const tpmg_facto
         if (L.d_ringc.p && tpmg::resid_restrict_T2_fusable(L.coef(nz))) {
           L.send3.alloc(deep_size(L, nz));
           L.recv3.alloc(deep_size(L, nz));
+          if (l < levels - 1 && !ctx->ipc) {  // coarse levels: f's halo posted early
+            L.sendF.alloc(faces);
+            L.recvF.alloc(faces);
+          }
         } else {
           L.d_ringc.reset();
         }

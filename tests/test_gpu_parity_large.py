@@ -80,3 +80,27 @@ def test_pcg_host_entry_k_fastest_matches_golden(gpu_ctx, name):
         assert float(np.sum(xk)).hex() == g["x_sum_hex"]
     finally:
         h.close()
+
+
+@pytest.mark.parametrize("name", ["cfg3", "cfg5t"])
+def test_decomposed_paths_match_golden_at_baseline_size(gpu_ctx, monkeypatch, name):
+    """The multi-rank device paths at BASELINE's sizes (TPMG_LOOPBACK=1: the rank is its own
+    periodic neighbour, so every face and two-cell halo is packed into receive buffers and read
+    back from them, the decomposed fused residual + restriction reads the coefficient ring, and
+    the multi-rank schedule runs) reproduce the one-rank oracle golden bit for bit -- the
+    decomposed code computes the reference's numbers, not just close ones."""
+    g = _golden(name)
+    P = synth.parity_problem(name)
+    monkeypatch.setenv("TPMG_LOOPBACK", "1")
+    h = tpmg.Hierarchy(gpu_ctx, P)
+    try:
+        f = h.field().upload(P.rhs())
+        x = h.field()
+        res = tpmg.pcg_solve(h, f, x, P.tol, 300)
+        assert res.status == 0 and res.iterations == g["iterations"]
+        assert [float(v).hex() for v in res.history] == g["history_hex"]
+        xs = x.download()
+        digest = hashlib.sha256(np.ascontiguousarray(xs, dtype="<f8").tobytes()).hexdigest()
+        assert digest == g["x_sha256_device_order"]
+    finally:
+        h.close()
