@@ -245,6 +245,12 @@ struct tpmg_hierarchy_s {
   DevBuf gathered;        // multi-rank: every rank's tile partials (gather_partials)
   int* d_err = nullptr;
   double* h_scal = nullptr;  // pinned
+  // one-rank PCG host loop: per-iteration scalars published into mapped pinned memory by the
+  // iteration's last kernel (k_pcg_publish); the host polls the sequence number
+  tpmg::PcgPublish* h_pub = nullptr;  // host view (cudaHostAllocMapped)
+  tpmg::PcgPublish* d_pub = nullptr;  // device alias
+  unsigned* d_seq = nullptr;
+  unsigned host_seq = 0;
   bool use_graphs = true;
   // Loopback halos (TPMG_LOOPBACK=1 at creation, one rank): every multi-rank device path —
   // face packing, the send -> recv transfer (here device copies onto this rank itself, the
@@ -256,9 +262,26 @@ struct tpmg_hierarchy_s {
   bool pcg_fused = false;  // PCG vector work fused into the finest-level smoother sweeps
   const double* f_first = nullptr;  // fused PCG: the right-hand side the first iteration reads
   bool fuse_rr = true;     // fused residual + transpose restriction (TPMG_FUSE_RR=0 disables)
-  // one graph per (iterate buffer, direction parity): key = (const char*)x + pcur
-  std::unordered_map<const void*, cudaGraphExec_t> iter_graphs;
-  std::unordered_map<const void*, int64_t> iter_graph_kernels;
+  // Captured PCG work, one graph per key: the prologue (r_0 dot, V-cycle, rho dot) per
+  // right-hand side, the first iteration per (right-hand side, iterate), the later iterations
+  // per (iterate, direction parity).  probes: the probe pairs every launch records.
+  struct GraphKey {
+    int tag;
+    const void* a;
+    const void* b;
+    bool operator==(const GraphKey& o) const { return tag == o.tag && a == o.a && b == o.b; }
+  };
+  struct GraphKeyHash {
+    size_t operator()(const GraphKey& k) const {
+      return std::hash<const void*>()(k.a) * 31u + std::hash<const void*>()(k.b) * 7u + (size_t)k.tag;
+    }
+  };
+  struct Graph {
+    cudaGraphExec_t exec = nullptr;
+    int64_t kernels = 0;
+    uint32_t probes = 0;
+  };
+  std::unordered_map<GraphKey, Graph, GraphKeyHash> graphs;
   // device-side PCG loop (iterations 2..): one graph per iterate buffer, a while-node whose body
   // holds two iterations (both direction parities), the second behind an if-node
   std::unordered_map<const void*, cudaGraphExec_t> loop_graphs;
@@ -279,7 +302,6 @@ struct tpmg_hierarchy_s {
   bool probe_on = false;
   Probe probes[kProbes];
   uint32_t probe_pending = 0;  // pairs recorded by the work queued since the last collection
-  std::unordered_map<const void*, uint32_t> iter_graph_probes;
   std::vector<void*> ipc_mapped;  // neighbours' receive buffers opened through CUDA IPC
   // exchange_f_async: per level, f ready on the main stream / halo landed on the side stream
   std::vector<cudaEvent_t> ev_fsrc, ev_fdone;
@@ -315,12 +337,14 @@ struct tpmg_hierarchy_s {
       if (pr.e0) cudaEventDestroy(pr.e0);
       if (pr.e1) cudaEventDestroy(pr.e1);
     }
-    for (auto& kv : iter_graphs) cudaGraphExecDestroy(kv.second);
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.exec);
     for (auto& kv : loop_graphs) cudaGraphExecDestroy(kv.second);
     if (d_loop) cudaFree(d_loop);
     if (h_loop) cudaFreeHost(h_loop);
     if (d_err) cudaFree(d_err);
     if (h_scal) cudaFreeHost(h_scal);
+    if (h_pub) cudaFreeHost(h_pub);
+    if (d_seq) cudaFree(d_seq);
   }
 };
 
@@ -954,7 +978,8 @@ void vcycle(tpmg_hierarchy h, int l, const double* f, double* A, double* B, bool
                                h->ctx->stream));
 }
 
-void sync_check(tpmg_hierarchy h) {
+// Synchronise and return the zero-pivot flag (all-reduced over the ranks) without acting on it.
+int sync_err(tpmg_hierarchy h) {
   // the error flag rides behind the queued work into pinned memory: one synchronisation
   int* h_err = reinterpret_cast<int*>(h->h_scal + 7);
   // multi-rank: every rank must take the same exit decision, or the ranks that did not see a
@@ -973,9 +998,16 @@ void sync_check(tpmg_hierarchy h) {
   CUDA_CHECK(cudaMemcpyAsync(h_err, h->d_err, sizeof(int), cudaMemcpyDeviceToHost,
                              h->ctx->stream));
   CUDA_CHECK(cudaStreamSynchronize(h->ctx->stream));
-  const int err = *h_err;
-  if (err) {
-    CUDA_CHECK(cudaMemsetAsync(h->d_err, 0, sizeof(int), h->ctx->stream));
+  return *h_err;
+}
+
+void clear_err(tpmg_hierarchy h) {
+  CUDA_CHECK(cudaMemsetAsync(h->d_err, 0, sizeof(int), h->ctx->stream));
+}
+
+void sync_check(tpmg_hierarchy h) {
+  if (sync_err(h)) {
+    clear_err(h);
     throw Error(TPMG_E_SINGULAR, "thomas_solve: zero pivot");
   }
 }
@@ -1004,29 +1036,35 @@ void same_hier(tpmg_hierarchy h, tpmg_field f) {
 // final iteration is applied after the loop (k_pcg_xfinal).  Every element is computed with
 // the same operations as the plain schedule: q = A p, p.q; x += a p, r -= a q, r.r;
 // z = V(r); r.z; p = z + b p.
-void pcg_iteration(tpmg_hierarchy h, double* x, bool first, int pc) {
+// part (fused A p schedule): 0 the whole iteration; 1 only its head, the direction update + A p
+// pass and its dot (run_iteration launches it eagerly, so that the launch of the graph holding
+// the rest overlaps that 0.9 ms pass instead of idling the GPU); 2 only the rest
+void pcg_iteration(tpmg_hierarchy h, double* x, bool first, int pc, int part = 0) {
   const int L = h->finest();
   const int64_t n = h->lv[L].plane * h->nz;
   tpmg_context ctx = h->ctx;
   if (h->pcg_fused) {
     if (!first && h->fused_ap) {
-      // direction update and A p in one pass; p_new goes to the other buffer
-      Level& F = h->lv[L];
-      double* po = h->pbuf(pc);
-      int nb = 0;
-      // halos of z and p_old (single rank: the periodic self views, no copy)
       // p_reuse: p_old's halo is already in set 1 (exchanged once, right after the pass that
       // formed it, for that iteration's r-update sweep)
       const bool p_reuse = h->multi() && h->q_in_sweep;
-      const Halo Hz = exchange(h, L, h->z.p, 0);
-      const Halo Hp = p_reuse ? halo_view(h, L, po, 1) : exchange(h, L, po, 1);
-      probe_begin(h, TPMG_K_PCG_DIRECTION);
-      tpmg::launch_pcg_ap(ctx->launch(), h->vcoef(), F.coef(h->nz), h->xi, h->z.p, Hz, po, Hp,
-                          h->pbuf(pc ^ 1),
-                          h->q_in_sweep ? nullptr : h->q.p, x, h->scal.p, h->partials.p, &nb);
-      probe_end(h, TPMG_K_PCG_DIRECTION);
-      tpmg::launch_copy_scalar(ctx->launch(), h->scal.p, 0, 3);
-      finish_dot(h, nb, 1, L);
+      if (part != 2) {
+        // direction update and A p in one pass; p_new goes to the other buffer
+        Level& F = h->lv[L];
+        double* po = h->pbuf(pc);
+        int nb = 0;
+        // halos of z and p_old (single rank: the periodic self views, no copy)
+        const Halo Hz = exchange(h, L, h->z.p, 0);
+        const Halo Hp = p_reuse ? halo_view(h, L, po, 1) : exchange(h, L, po, 1);
+        probe_begin(h, TPMG_K_PCG_DIRECTION);
+        tpmg::launch_pcg_ap(ctx->launch(), h->vcoef(), F.coef(h->nz), h->xi, h->z.p, Hz, po, Hp,
+                            h->pbuf(pc ^ 1),
+                            h->q_in_sweep ? nullptr : h->q.p, x, h->scal.p, h->partials.p, &nb);
+        probe_end(h, TPMG_K_PCG_DIRECTION);
+        tpmg::launch_copy_scalar(ctx->launch(), h->scal.p, 0, 3);
+        finish_dot(h, nb, 1, L);
+      }
+      if (part == 1) return;
       Halo Hpn;
       if (p_reuse) Hpn = exchange(h, L, h->pbuf(pc ^ 1), 1);
       vcycle(h, L, h->r.p, h->z.p, h->tmp.p, true, true,
@@ -1055,41 +1093,95 @@ void pcg_iteration(tpmg_hierarchy h, double* x, bool first, int pc) {
   tpmg::launch_copy_scalar(ctx->launch(), h->scal.p, 0, 3);
 }
 
-void run_iteration(tpmg_hierarchy h, double* x, bool first) {
+// Wait for the iteration's k_pcg_publish: poll the sequence number in mapped pinned memory
+// (the host wakes as soon as it lands, no stream synchronisation); every few thousand polls ask
+// the stream whether it failed.  Then the scalars go to h_scal and a zero pivot raises the
+// reference's singular_error, as sync_check does.
+void wait_publish(tpmg_hierarchy h) {
+  const unsigned want = ++h->host_seq;
+  volatile unsigned* seq = &h->h_pub->seq;
+  for (uint64_t spin = 0; *seq != want; ++spin) {
+    if ((spin & 4095) == 4095) {
+      const cudaError_t e = cudaStreamQuery(h->ctx->stream);
+      if (e != cudaSuccess && e != cudaErrorNotReady) CUDA_CHECK(e);
+      if (e == cudaSuccess && *seq != want)
+        throw Error(TPMG_E_CUDA, "pcg: iteration scalars were not published");
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+  for (int i = 0; i < 4; ++i) h->h_scal[i] = h->h_pub->s[i];
+  if (h->h_pub->err) {
+    CUDA_CHECK(cudaMemsetAsync(h->d_err, 0, sizeof(int), h->ctx->stream));
+    CUDA_CHECK(cudaStreamSynchronize(h->ctx->stream));
+    throw Error(TPMG_E_SINGULAR, "thomas_solve: zero pivot");
+  }
+}
+
+// the iteration's scalars to the host through k_pcg_publish (one rank; see wait_publish)
+bool publish_ok(tpmg_hierarchy h) { return h->h_pub && !h->multi(); }
+void publish(tpmg_hierarchy h) {
+  if (publish_ok(h))
+    tpmg::launch_pcg_publish(h->ctx->launch(), h->scal.p, h->d_err, h->d_seq, h->d_pub);
+}
+
+// Run fn() as the graph cached under key (captured on first use); fn() eagerly where graphs
+// are off or the transport orders its exchanges on the host (IPC).
+template <class Fn>
+void run_graph(tpmg_hierarchy h, const tpmg_hierarchy_s::GraphKey& key, Fn&& fn) {
   tpmg_context ctx = h->ctx;
-  const int pc = h->pcur;
-  // the fused A p pass moves the direction to the other buffer
-  if (h->pcg_fused && h->fused_ap && !first) h->pcur ^= 1;
-  if (!h->use_graphs || ctx->ipc || (first && h->pcg_fused)) {  // IPC: host-ordered exchanges
-    pcg_iteration(h, x, first, pc);
+  if (!h->use_graphs || ctx->ipc) {
+    fn();
     return;
   }
-  const void* key = reinterpret_cast<const char*>(x) + pc;
-  auto it = h->iter_graphs.find(key);
-  if (it == h->iter_graphs.end()) {
+  auto it = h->graphs.find(key);
+  if (it == h->graphs.end()) {
     cudaGraph_t g;
     const int64_t before = ctx->launches;
+    const uint32_t eager_probes = h->probe_pending;  // recorded eagerly before the capture
+    h->probe_pending = 0;
     CUDA_CHECK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
     try {
-      pcg_iteration(h, x, false, pc);
+      fn();
     } catch (...) {
       cudaStreamEndCapture(ctx->stream, &g);
       throw;
     }
     CUDA_CHECK(cudaStreamEndCapture(ctx->stream, &g));
-    const int64_t nk = ctx->launches - before;
+    tpmg_hierarchy_s::Graph G;
+    G.kernels = ctx->launches - before;
     ctx->launches = before;
-    h->iter_graph_probes[key] = h->probe_pending;  // recorded by every launch of this graph
-    h->probe_pending = 0;
-    cudaGraphExec_t ge;
-    CUDA_CHECK(cudaGraphInstantiate(&ge, g, 0));
+    G.probes = h->probe_pending;  // recorded by every launch of this graph
+    h->probe_pending = eager_probes;
+    CUDA_CHECK(cudaGraphInstantiate(&G.exec, g, 0));
     cudaGraphDestroy(g);
-    it = h->iter_graphs.emplace(key, ge).first;
-    h->iter_graph_kernels[key] = nk;
+    it = h->graphs.emplace(key, G).first;
   }
-  CUDA_CHECK(cudaGraphLaunch(it->second, ctx->stream));
-  ctx->launches += h->iter_graph_kernels[key];
-  h->probe_pending |= h->iter_graph_probes[key];
+  CUDA_CHECK(cudaGraphLaunch(it->second.exec, ctx->stream));
+  ctx->launches += it->second.kernels;
+  h->probe_pending |= it->second.probes;
+}
+
+enum GraphTag { G_PROLOGUE = 1, G_FIRST = 2, G_ITER = 3 };
+
+void run_iteration(tpmg_hierarchy h, double* x, bool first) {
+  const int pc = h->pcur;
+  // the fused A p pass moves the direction to the other buffer
+  if (h->pcg_fused && h->fused_ap && !first) h->pcur ^= 1;
+  if (first) {  // the fused schedule's first iteration reads the right-hand side f_first
+    run_graph(h, {G_FIRST, x, h->pcg_fused ? h->f_first : nullptr}, [&] {
+      pcg_iteration(h, x, true, pc);
+      publish(h);
+    });
+    return;
+  }
+  // fused A p schedule: the head pass eagerly, the rest as the graph (whose launch then
+  // overlaps the head instead of idling the GPU)
+  const bool split = h->pcg_fused && h->fused_ap && h->use_graphs && !h->ctx->ipc;
+  if (split) pcg_iteration(h, x, false, pc, 1);
+  run_graph(h, {G_ITER, x, h->pbuf(pc)}, [&] {  // keyed by the direction parity
+    pcg_iteration(h, x, false, pc, split ? 2 : 0);
+    publish(h);
+  });
 }
 
 // Opt-in (TPMG_DEVLOOP=1, read per solve): bench.py measures the same solve time either way
@@ -2218,28 +2310,45 @@ int tpmg_pcg(tpmg_hierarchy h, tpmg_field f, tpmg_field x, double tol, int max_i
     tpmg_context ctx = h->ctx;
     const int64_t n = f->buf.n;
     cudaStream_t s = ctx->stream;
+    if (!h->h_pub && !h->multi()) {  // before any iteration graph is captured
+      CUDA_CHECK(cudaHostAlloc(&h->h_pub, sizeof(tpmg::PcgPublish), cudaHostAllocMapped));
+      std::memset(h->h_pub, 0, sizeof(tpmg::PcgPublish));
+      CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->d_pub), h->h_pub, 0));
+      CUDA_CHECK(cudaMalloc(&h->d_seq, sizeof(unsigned)));
+      CUDA_CHECK(cudaMemsetAsync(h->d_seq, 0, sizeof(unsigned), s));
+      h->host_seq = 0;
+    }
     CUDA_CHECK(cudaMemsetAsync(x->buf.p, 0, n * 8, s));
     // r_0 = f.  The fused schedule never copies it: the prologue reads f, and the first
     // iteration's pre-sweep reads f and writes r_1 = f - alpha q into r (vcycle f_pre)
-    const double* r0p = f->buf.p;
-    if (h->pcg_fused) {
-      h->f_first = f->buf.p;
-    } else {
-      CUDA_CHECK(cudaMemcpyAsync(h->r.p, f->buf.p, n * 8, cudaMemcpyDeviceToDevice, s));
-      r0p = h->r.p;
-    }
-    dot_into(h, L, r0p, r0p, 2);
-    const double r0 = std::sqrt(read_scalar(h, 2));
+    const double* r0p = h->pcg_fused ? f->buf.p : h->r.p;
+    if (h->pcg_fused) h->f_first = f->buf.p;
+    // prologue, one graph per right-hand side: |r_0|^2; z_0 = M r_0 straight into the direction
+    // buffer (p_1 = z_0; the first iteration's V-cycle writes z itself: no 1 GB device copy);
+    // rho_0 = r_0.z_0 -- then one synchronisation reads both scalars
+    run_graph(h, {G_PROLOGUE, f->buf.p, nullptr}, [&] {
+      if (!h->pcg_fused)
+        CUDA_CHECK(cudaMemcpyAsync(h->r.p, f->buf.p, n * 8, cudaMemcpyDeviceToDevice, s));
+      dot_into(h, L, r0p, r0p, 2);
+      vcycle(h, L, r0p, h->p.p, h->tmp.p, true);
+      dot_into(h, L, r0p, h->p.p, 0);
+    });
+    h->pcur = 0;
+    CUDA_CHECK(cudaMemcpyAsync(h->h_scal, h->scal.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    const int err0 = sync_err(h);
+    const double r0 = std::sqrt(h->h_scal[2]);
     if (res_hist) res_hist[0] = r0;
     *iters = 0;
     *solve_status = TPMG_OK;
-    if (r0 == 0.0) return;
-    // z_0 = M r_0 goes straight into the direction buffer (p_1 = z_0; the first iteration's
-    // V-cycle writes z itself): no 1 GB device copy
-    vcycle(h, L, r0p, h->p.p, h->tmp.p, true);
-    h->pcur = 0;
-    dot_into(h, L, r0p, h->p.p, 0);
-    if (!(read_scalar(h, 0) > 0.0)) {
+    if (r0 == 0.0) {  // x = 0 is the solution; the V-cycle of a zero right-hand side is moot
+      if (err0) clear_err(h);
+      return;
+    }
+    if (err0) {
+      clear_err(h);
+      throw Error(TPMG_E_SINGULAR, "thomas_solve: zero pivot");
+    }
+    if (!(h->h_scal[0] > 0.0)) {
       *solve_status = TPMG_BREAKDOWN;
       return;
     }
@@ -2284,8 +2393,12 @@ int tpmg_pcg(tpmg_hierarchy h, tpmg_field f, tpmg_field x, double tol, int max_i
       const auto t_a = std::chrono::steady_clock::now();
       run_iteration(h, x->buf.p, it == 1);
       const auto t_b = std::chrono::steady_clock::now();
-      CUDA_CHECK(cudaMemcpyAsync(h->h_scal, h->scal.p, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
-      sync_check(h);
+      if (publish_ok(h)) {
+        wait_publish(h);
+      } else {
+        CUDA_CHECK(cudaMemcpyAsync(h->h_scal, h->scal.p, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
+        sync_check(h);
+      }
       probe_collect(h);
       if (debug_timing) {  // TPMG_DEBUG_TIMING=1: host time to queue / wait for each iteration
         const auto t_c = std::chrono::steady_clock::now();
@@ -2578,10 +2691,8 @@ int tpmg_kernel_probe(tpmg_hierarchy h, int enable) {
   return guard(h->ctx, [&] {
     if ((enable != 0) != h->probe_on) {  // cached iteration graphs carry (or lack) the probes
       CUDA_CHECK(cudaStreamSynchronize(h->ctx->stream));
-      for (auto& kv : h->iter_graphs) cudaGraphExecDestroy(kv.second);
-      h->iter_graphs.clear();
-      h->iter_graph_kernels.clear();
-      h->iter_graph_probes.clear();
+      for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second.exec);
+      h->graphs.clear();
       for (auto& kv : h->loop_graphs) cudaGraphExecDestroy(kv.second);
       h->loop_graphs.clear();
     }

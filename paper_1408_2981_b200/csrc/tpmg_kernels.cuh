@@ -169,6 +169,16 @@ struct PcgLoop {
 };
 void launch_pcg_check(const Launch& L, const double* scal, double* hist, PcgLoop* st,
                       unsigned long long hw, unsigned long long hi, int use_hi);
+// End of a PCG iteration (host loop, one rank): the scalars the convergence test reads and the
+// zero-pivot flag written into mapped pinned host memory, then a sequence number behind a
+// system-scope fence; the host polls the number instead of copying and synchronising.
+struct PcgPublish {
+  double s[4];
+  int err;
+  unsigned seq;
+};
+void launch_pcg_publish(const Launch& L, const double* scal, const int* err, unsigned* dseq,
+                        PcgPublish* hp);
 // levels whose sweeps take the pre-factorised warp-per-column path when factors exist
 bool jacobi_wants_factors(const LevelCoef& C);
 // one-time device constants (L2 cache policies); called at context creation, outside any

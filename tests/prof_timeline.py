@@ -28,6 +28,7 @@ def main():
     P = synth.baseline_config(int(os.environ.get("TPMG_CFG", "3")))
     ctx = tpmg.Context()
     h = tpmg.Hierarchy(ctx, P)
+    h.set_use_graphs(os.environ.get("TPMG_GRAPHS", "1") == "1")
     f = h.field().upload(P.rhs())
     x = h.field()
     for _ in range(2):
