@@ -277,6 +277,16 @@ int tpmg_solver_counts(tpmg_hierarchy h, int64_t* n_precond, int64_t* n_matvec);
 int tpmg_pcg_host(tpmg_hierarchy h, const double* f_host, double* x_host, int layout, double tol,
                   int max_iter, double* res_hist, int* iters, int* solve_status);
 
+/* End-to-end solves of `count` independent right-hand sides f_hosts[i] -> x_hosts[i] (layout),
+ * the host<->device transfers overlapped with the solves: while right-hand side i is solved,
+ * right-hand side i+1 is uploaded and solution i-1 downloaded on a copy stream (double-buffered
+ * device fields; pinned host buffers for the copies to overlap).  Each solve is tpmg_pcg's, so
+ * the results equal `count` tpmg_pcg_host calls bit for bit.  res_hist: count x (max_iter+1)
+ * or NULL; iters, solve_status: count entries. */
+int tpmg_pcg_host_batch(tpmg_hierarchy h, int count, const double* const* f_hosts,
+                        double* const* x_hosts, int layout, double tol, int max_iter,
+                        double* res_hist, int* iters, int* solve_status);
+
 /* ---- profile files: save_profiles / load_profiles (profile_io.hpp:125-242) ------------------ */
 /* The reference's JSON profile format, byte for byte as its writer (nlohmann dump(1): keys
  * sorted, shortest round-trip doubles, non-finite -> null): format_version 1, kind "factorized" |

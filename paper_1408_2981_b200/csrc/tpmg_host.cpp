@@ -251,6 +251,14 @@ struct tpmg_hierarchy_s {
   tpmg::PcgPublish* d_pub = nullptr;  // device alias
   unsigned* d_seq = nullptr;
   unsigned host_seq = 0;
+  // tpmg_pcg_host_batch: double-buffered finest-level right-hand sides and iterates, staging
+  // buffers of the layout permutations, the copy stream and its events (allocated on first use)
+  struct Batch {
+    DevBuf F[2], X[2], stage_in, stage_out;
+    cudaStream_t copy = nullptr;
+    cudaEvent_t up[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr},
+                down[2] = {nullptr, nullptr};
+  } bat;
   bool use_graphs = true;
   // Loopback halos (TPMG_LOOPBACK=1 at creation, one rank): every multi-rank device path —
   // face packing, the send -> recv transfer (here device copies onto this rank itself, the
@@ -331,6 +339,10 @@ struct tpmg_hierarchy_s {
     d_vx.upload(vx.data(), vx.size());
   }
   ~tpmg_hierarchy_s() {
+    for (int i = 0; i < 2; ++i)
+      for (cudaEvent_t e : {bat.up[i], bat.done[i], bat.down[i]})
+        if (e) cudaEventDestroy(e);
+    if (bat.copy) cudaStreamDestroy(bat.copy);
     for (cudaEvent_t e : ev_fsrc) cudaEventDestroy(e);
     for (cudaEvent_t e : ev_fdone) cudaEventDestroy(e);
     for (auto& pr : probes) {
@@ -1097,7 +1109,7 @@ void pcg_iteration(tpmg_hierarchy h, double* x, bool first, int pc, int part = 0
 // (the host wakes as soon as it lands, no stream synchronisation); every few thousand polls ask
 // the stream whether it failed.  Then the scalars go to h_scal and a zero pivot raises the
 // reference's singular_error, as sync_check does.
-void wait_publish(tpmg_hierarchy h) {
+int wait_publish_raw(tpmg_hierarchy h) {
   const unsigned want = ++h->host_seq;
   volatile unsigned* seq = &h->h_pub->seq;
   for (uint64_t spin = 0; *seq != want; ++spin) {
@@ -1110,7 +1122,10 @@ void wait_publish(tpmg_hierarchy h) {
   }
   std::atomic_thread_fence(std::memory_order_acquire);
   for (int i = 0; i < 4; ++i) h->h_scal[i] = h->h_pub->s[i];
-  if (h->h_pub->err) {
+  return h->h_pub->err;
+}
+void wait_publish(tpmg_hierarchy h) {
+  if (wait_publish_raw(h)) {
     CUDA_CHECK(cudaMemsetAsync(h->d_err, 0, sizeof(int), h->ctx->stream));
     CUDA_CHECK(cudaStreamSynchronize(h->ctx->stream));
     throw Error(TPMG_E_SINGULAR, "thomas_solve: zero pivot");
@@ -2300,15 +2315,12 @@ int tpmg_measure_cycle_rate(tpmg_hierarchy h, tpmg_field f, int n_cycles, double
   });
 }
 
-int tpmg_pcg(tpmg_hierarchy h, tpmg_field f, tpmg_field x, double tol, int max_iter,
-             double* res_hist, int* iters, int* solve_status) {
-  return guard(h->ctx, [&] {
-    same_hier(h, f); same_hier(h, x);
+namespace {
+// The PCG solve of tpmg_pcg on raw finest-level device buffers f (read) and x (written).
+void pcg_impl(tpmg_hierarchy h, const double* fp, double* xp, int64_t n, double tol, int max_iter,
+              double* res_hist, int* iters, int* solve_status) {
     const int L = h->finest();
-    if (f->level != L || x->level != L) throw Error(TPMG_E_SHAPE, "pcg: fields must be finest");
-    if (max_iter < 0) throw Error(TPMG_E_CONFIG, "max_iter must be >= 0");
     tpmg_context ctx = h->ctx;
-    const int64_t n = f->buf.n;
     cudaStream_t s = ctx->stream;
     if (!h->h_pub && !h->multi()) {  // before any iteration graph is captured
       CUDA_CHECK(cudaHostAlloc(&h->h_pub, sizeof(tpmg::PcgPublish), cudaHostAllocMapped));
@@ -2318,24 +2330,32 @@ int tpmg_pcg(tpmg_hierarchy h, tpmg_field f, tpmg_field x, double tol, int max_i
       CUDA_CHECK(cudaMemsetAsync(h->d_seq, 0, sizeof(unsigned), s));
       h->host_seq = 0;
     }
-    CUDA_CHECK(cudaMemsetAsync(x->buf.p, 0, n * 8, s));
+    CUDA_CHECK(cudaMemsetAsync(xp, 0, n * 8, s));
     // r_0 = f.  The fused schedule never copies it: the prologue reads f, and the first
     // iteration's pre-sweep reads f and writes r_1 = f - alpha q into r (vcycle f_pre)
-    const double* r0p = h->pcg_fused ? f->buf.p : h->r.p;
-    if (h->pcg_fused) h->f_first = f->buf.p;
+    const double* r0p = h->pcg_fused ? fp : h->r.p;
+    if (h->pcg_fused) h->f_first = fp;
     // prologue, one graph per right-hand side: |r_0|^2; z_0 = M r_0 straight into the direction
     // buffer (p_1 = z_0; the first iteration's V-cycle writes z itself: no 1 GB device copy);
     // rho_0 = r_0.z_0 -- then one synchronisation reads both scalars
-    run_graph(h, {G_PROLOGUE, f->buf.p, nullptr}, [&] {
+    run_graph(h, {G_PROLOGUE, fp, nullptr}, [&] {
       if (!h->pcg_fused)
-        CUDA_CHECK(cudaMemcpyAsync(h->r.p, f->buf.p, n * 8, cudaMemcpyDeviceToDevice, s));
+        CUDA_CHECK(cudaMemcpyAsync(h->r.p, fp, n * 8, cudaMemcpyDeviceToDevice, s));
       dot_into(h, L, r0p, r0p, 2);
       vcycle(h, L, r0p, h->p.p, h->tmp.p, true);
       dot_into(h, L, r0p, h->p.p, 0);
     });
     h->pcur = 0;
-    CUDA_CHECK(cudaMemcpyAsync(h->h_scal, h->scal.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
-    const int err0 = sync_err(h);
+    // (published through mapped memory where possible: a copy-engine readback would queue
+    // behind the large device-to-host copies of tpmg_pcg_host_batch)
+    int err0 = 0;
+    if (publish_ok(h)) {
+      publish(h);
+      err0 = wait_publish_raw(h);
+    } else {
+      CUDA_CHECK(cudaMemcpyAsync(h->h_scal, h->scal.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+      err0 = sync_err(h);
+    }
     const double r0 = std::sqrt(h->h_scal[2]);
     if (res_hist) res_hist[0] = r0;
     *iters = 0;
@@ -2355,8 +2375,13 @@ int tpmg_pcg(tpmg_hierarchy h, tpmg_field f, tpmg_field x, double tol, int max_i
     // fused schedule: the last iteration's x += alpha p is still pending when the loop ends
     auto finish_x = [&] {
       if (h->pcg_fused && *iters > 0) {  // max_iter = 0: no pending update, x stays 0
-        tpmg::launch_pcg_xfinal(ctx->launch(), n, h->scal.p, h->pbuf(h->pcur), x->buf.p);
-        sync_check(h);
+        tpmg::launch_pcg_xfinal(ctx->launch(), n, h->scal.p, h->pbuf(h->pcur), xp);
+        if (publish_ok(h)) {
+          publish(h);
+          wait_publish(h);
+        } else {
+          sync_check(h);
+        }
       }
     };
     static const bool debug_timing = [] {
@@ -2366,7 +2391,7 @@ int tpmg_pcg(tpmg_hierarchy h, tpmg_field f, tpmg_field x, double tol, int max_i
     for (int it = 1; it <= max_iter; ++it) {
       if (it == 2 && device_loop_ok(h, max_iter)) {
         // iterations 2.. as one graph launch: the convergence test runs on the device
-        cudaGraphExec_t ge = loop_graph(h, x->buf.p);
+        cudaGraphExec_t ge = loop_graph(h, xp);
         *h->h_loop = tpmg::PcgLoop{r0, tol, max_iter, 1, 1, 0};
         CUDA_CHECK(cudaMemcpyAsync(h->d_loop, h->h_loop, sizeof(tpmg::PcgLoop),
                                    cudaMemcpyHostToDevice, s));
@@ -2391,7 +2416,7 @@ int tpmg_pcg(tpmg_hierarchy h, tpmg_field f, tpmg_field x, double tol, int max_i
         }
       }
       const auto t_a = std::chrono::steady_clock::now();
-      run_iteration(h, x->buf.p, it == 1);
+      run_iteration(h, xp, it == 1);
       const auto t_b = std::chrono::steady_clock::now();
       if (publish_ok(h)) {
         wait_publish(h);
@@ -2431,6 +2456,92 @@ int tpmg_pcg(tpmg_hierarchy h, tpmg_field f, tpmg_field x, double tol, int max_i
     }
     *solve_status = TPMG_NOT_CONVERGED;
     finish_x();
+}
+}  // namespace
+
+int tpmg_pcg(tpmg_hierarchy h, tpmg_field f, tpmg_field x, double tol, int max_iter,
+             double* res_hist, int* iters, int* solve_status) {
+  return guard(h->ctx, [&] {
+    same_hier(h, f); same_hier(h, x);
+    const int L = h->finest();
+    if (f->level != L || x->level != L) throw Error(TPMG_E_SHAPE, "pcg: fields must be finest");
+    if (max_iter < 0) throw Error(TPMG_E_CONFIG, "max_iter must be >= 0");
+    pcg_impl(h, f->buf.p, x->buf.p, f->buf.n, tol, max_iter, res_hist, iters, solve_status);
+  });
+}
+
+// Solves `count` independent right-hand sides from host memory, the transfers overlapped with
+// the solves: while right-hand side i is solved on the library stream, the copy stream uploads
+// (and permutes) right-hand side i+1 into the other device buffer and permutes and downloads
+// solution i-1.  Each solve is tpmg_pcg's, so every solution, history and status is bitwise
+// the one-at-a-time result.  Host buffers should be pinned for the copies to overlap.
+int tpmg_pcg_host_batch(tpmg_hierarchy h, int count, const double* const* f_hosts,
+                        double* const* x_hosts, int layout, double tol, int max_iter,
+                        double* res_hist, int* iters, int* solve_status) {
+  return guard(h->ctx, [&] {
+    if (count < 0 || max_iter < 0) throw Error(TPMG_E_CONFIG, "count and max_iter must be >= 0");
+    if (count > 0 && (!f_hosts || !x_hosts || !iters || !solve_status))
+      throw Error(TPMG_E_CONFIG, "null argument");
+    if (layout != TPMG_LAYOUT_X_FASTEST && layout != TPMG_LAYOUT_K_FASTEST)
+      throw Error(TPMG_E_CONFIG, "unknown layout");
+    tpmg_context ctx = h->ctx;
+    const int L = h->finest();
+    const int64_t n = h->lv[L].plane * h->nz;
+    auto& B = h->bat;
+    if (!B.copy) {
+      CUDA_CHECK(cudaStreamCreateWithFlags(&B.copy, cudaStreamNonBlocking));
+      for (int i = 0; i < 2; ++i) {
+        B.F[i].alloc(n);
+        B.X[i].alloc(n);
+        CUDA_CHECK(cudaEventCreateWithFlags(&B.up[i], cudaEventDisableTiming));
+        CUDA_CHECK(cudaEventCreateWithFlags(&B.done[i], cudaEventDisableTiming));
+        CUDA_CHECK(cudaEventCreateWithFlags(&B.down[i], cudaEventDisableTiming));
+      }
+      B.stage_in.alloc(n);
+      B.stage_out.alloc(n);
+    }
+    const tpmg::Launch cl{B.copy, &ctx->launches};
+    const bool kf = layout == TPMG_LAYOUT_K_FASTEST;
+    // the copy stream's first work may not overtake anything queued on the library stream
+    CUDA_CHECK(cudaEventRecord(B.done[0], ctx->stream));
+    CUDA_CHECK(cudaEventRecord(B.done[1], ctx->stream));
+    CUDA_CHECK(cudaEventRecord(B.down[0], ctx->stream));
+    CUDA_CHECK(cudaEventRecord(B.down[1], ctx->stream));
+    auto upload = [&](int i) {  // f_i -> F[i % 2], after the solve that last read F[i % 2]
+      const int b = i % 2;
+      CUDA_CHECK(cudaStreamWaitEvent(B.copy, B.done[b], 0));
+      if (kf) {
+        CUDA_CHECK(cudaMemcpyAsync(B.stage_in.p, f_hosts[i], n * 8, cudaMemcpyHostToDevice, B.copy));
+        tpmg::launch_kfast_to_xfast(cl, h->lv[L].plane, h->nz, B.stage_in.p, B.F[b].p);
+      } else {
+        CUDA_CHECK(cudaMemcpyAsync(B.F[b].p, f_hosts[i], n * 8, cudaMemcpyHostToDevice, B.copy));
+      }
+      CUDA_CHECK(cudaEventRecord(B.up[b], B.copy));
+    };
+    auto download = [&](int i) {  // X[i % 2] -> x_i, after solve i
+      const int b = i % 2;
+      CUDA_CHECK(cudaStreamWaitEvent(B.copy, B.done[b], 0));
+      if (kf) {
+        tpmg::launch_xfast_to_kfast(cl, h->lv[L].plane, h->nz, B.X[b].p, B.stage_out.p);
+        CUDA_CHECK(cudaMemcpyAsync(x_hosts[i], B.stage_out.p, n * 8, cudaMemcpyDeviceToHost, B.copy));
+      } else {
+        CUDA_CHECK(cudaMemcpyAsync(x_hosts[i], B.X[b].p, n * 8, cudaMemcpyDeviceToHost, B.copy));
+      }
+      CUDA_CHECK(cudaEventRecord(B.down[b], B.copy));
+    };
+    if (count > 0) upload(0);
+    for (int i = 0; i < count; ++i) {
+      const int b = i % 2;
+      if (i + 1 < count) upload(i + 1);  // overlaps solve i
+      CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, B.up[b], 0));
+      CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, B.down[b], 0));  // solution i-2 is out of X[b]
+      pcg_impl(h, B.F[b].p, B.X[b].p, n, tol, max_iter,
+               res_hist ? res_hist + (int64_t)i * (max_iter + 1) : nullptr, iters + i,
+               solve_status + i);
+      CUDA_CHECK(cudaEventRecord(B.done[b], ctx->stream));
+      download(i);  // overlaps solve i+1
+    }
+    CUDA_CHECK(cudaStreamSynchronize(B.copy));
   });
 }
 

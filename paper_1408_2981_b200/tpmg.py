@@ -490,6 +490,27 @@ def pcg_solve_host(h: Hierarchy, f_host: np.ndarray, tol: float, max_iter: int =
     return x, SolveResult(it.value, st.value, hist[: it.value + 1].copy(), 0.0)
 
 
+def pcg_solve_host_batch(h: Hierarchy, f_hosts, x_hosts, tol: float, max_iter: int = 500,
+                         layout: int = X_FASTEST):
+    """End-to-end solves of several right-hand sides with the transfers overlapped
+    (tpmg_pcg_host_batch): f_hosts[i] -> x_hosts[i] (contiguous float64 arrays, pinned for the
+    copies to overlap).  Returns one SolveResult per right-hand side."""
+    count = len(f_hosts)
+    if len(x_hosts) != count:
+        raise ValueError("f_hosts and x_hosts differ in length")
+    for a in list(f_hosts) + list(x_hosts):
+        if a.dtype != np.float64 or not a.flags.c_contiguous:
+            raise ValueError("host buffers must be contiguous float64")
+    fp = (_capi._D * count)(*[_p(a) for a in f_hosts])
+    xp = (_capi._D * count)(*[_p(a) for a in x_hosts])
+    hist = np.zeros((count, max_iter + 1))
+    it = (C.c_int * count)()
+    st = (C.c_int * count)()
+    h.ctx._check(h.lib.tpmg_pcg_host_batch(h._h, count, fp, xp, layout, C.c_double(tol), max_iter,
+                                           _p(hist), it, st))
+    return [SolveResult(it[i], st[i], hist[i, : it[i] + 1].copy(), 0.0) for i in range(count)]
+
+
 # ---- profile files: save_profiles / load_profiles (profile_io.hpp:125-242) ----------------------
 
 PROFILE_FACTORIZED, PROFILE_FULL = 0, 2

@@ -104,3 +104,23 @@ def test_decomposed_paths_match_golden_at_baseline_size(gpu_ctx, monkeypatch, na
         assert digest == g["x_sha256_device_order"]
     finally:
         h.close()
+
+
+def test_host_batch_matches_golden_at_baseline_size(gpu_ctx):
+    """The overlapped batch entry (bench.py's e2e path) at config 3: every solve of the batch
+    reproduces the oracle golden (pinned host buffers, the reference's k-fastest layout)."""
+    import torch
+
+    g = _golden("cfg3")
+    P = synth.parity_problem("cfg3")
+    h = tpmg.Hierarchy(gpu_ctx, P)
+    try:
+        fk = torch.from_numpy(synth.x_fastest_to_k_fastest(P.rhs()).reshape(-1)).pin_memory().numpy()
+        xs = [torch.empty(fk.size, dtype=torch.float64).pin_memory().numpy() for _ in range(3)]
+        res = tpmg.pcg_solve_host_batch(h, [fk] * 3, xs, P.tol, 300, layout=tpmg.K_FASTEST)
+        for r, xk in zip(res, xs):
+            assert r.iterations == g["iterations"]
+            assert [float(v).hex() for v in r.history] == g["history_hex"]
+            assert float(np.sum(xk)).hex() == g["x_sum_hex"]
+    finally:
+        h.close()
