@@ -241,6 +241,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--max-iter", type=int, default=500)
     ap.add_argument("--no-coef", action="store_true", help="skip the coefficient-storage comparison")
+    ap.add_argument("--global-coarsening", action="store_true",
+                    help="config 4w: coarsen the global grid as deep as the decomposition allows "
+                         "instead of BASELINE's 8x8 per GPU tile (iterations stay ~11-13 at any N)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -258,6 +261,9 @@ def main():
         dist.init_process_group("gloo", init_method="env://")
     px, py = proc_grid(world)
     P, workload, scaling, golden_name = make_problem(args.config, px, py)
+    if args.global_coarsening and args.config in ("3", "4w") and world > 1:
+        P.depth = 0
+        workload += ", global coarsening"
     torch.cuda.set_device(local)
 
     nccl_id = None
