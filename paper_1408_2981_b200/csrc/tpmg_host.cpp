@@ -930,6 +930,9 @@ void vcycle(tpmg_hierarchy h, int l, const double* f, double* A, double* B, bool
   Level& L = h->lv[l];
   const int64_t n = L.plane * h->nz;
   const int npre = h->nu_pre[l], npost = h->nu_post[l], total = npre + npost;
+  // an early-posted f halo (exchange_f_async) is consumed by the residual + restriction of the
+  // same V-cycle; drop any left over by a V-cycle an error interrupted
+  for (int m = 0; m < l; ++m) h->lv[m].f_pending = false;
   double* cur = A;
   auto other = [&](double* c) { return c == A ? B : A; };
   int s0 = 0;
@@ -2718,6 +2721,7 @@ int tpmg_time_kernel(tpmg_hierarchy h, int kernel_id, int level, int reps, doubl
     const bool transfer = kernel_id == TPMG_K_RESID_RESTRICT || kernel_id == TPMG_K_PROLONG_ADD ||
                           kernel_id == TPMG_K_RESTRICT;
     if (transfer && level < 1) throw Error(TPMG_E_SHAPE, "transfers need a fine level >= 1");
+    for (Level& Lm : h->lv) Lm.f_pending = false;  // no early-posted halo belongs to these calls
     Level& L = h->lv[level];
     const int64_t n = L.plane * h->nz;
     const bool pcg_kernel = kernel_id == TPMG_K_PCG_DIRECTION || kernel_id == TPMG_K_PCG_RUPDATE ||
