@@ -2532,17 +2532,23 @@ int tpmg_pcg_host_batch(tpmg_hierarchy h, int count, const double* const* f_host
       }
       CUDA_CHECK(cudaEventRecord(B.down[b], B.copy));
     };
-    if (count > 0) upload(0);
-    for (int i = 0; i < count; ++i) {
-      const int b = i % 2;
-      if (i + 1 < count) upload(i + 1);  // overlaps solve i
-      CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, B.up[b], 0));
-      CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, B.down[b], 0));  // solution i-2 is out of X[b]
-      pcg_impl(h, B.F[b].p, B.X[b].p, n, tol, max_iter,
-               res_hist ? res_hist + (int64_t)i * (max_iter + 1) : nullptr, iters + i,
-               solve_status + i);
-      CUDA_CHECK(cudaEventRecord(B.done[b], ctx->stream));
-      download(i);  // overlaps solve i+1
+    try {
+      if (count > 0) upload(0);
+      for (int i = 0; i < count; ++i) {
+        const int b = i % 2;
+        if (i + 1 < count) upload(i + 1);  // overlaps solve i
+        CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, B.up[b], 0));
+        CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, B.down[b], 0));  // solution i-2 left X[b]
+        pcg_impl(h, B.F[b].p, B.X[b].p, n, tol, max_iter,
+                 res_hist ? res_hist + (int64_t)i * (max_iter + 1) : nullptr, iters + i,
+                 solve_status + i);
+        CUDA_CHECK(cudaEventRecord(B.done[b], ctx->stream));
+        download(i);  // overlaps solve i+1
+      }
+    } catch (...) {
+      // no copy may still touch the caller's host buffers once the error is returned
+      cudaStreamSynchronize(B.copy);
+      throw;
     }
     CUDA_CHECK(cudaStreamSynchronize(B.copy));
   });
