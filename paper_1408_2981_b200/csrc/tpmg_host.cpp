@@ -1346,7 +1346,11 @@ int tpmg_init(const tpmg_context_params* prm, tpmg_context* out) {
       ncclUniqueId id;
       std::memcpy(&id, prm->nccl_id, sizeof(id));
       NCCL_CHECK(g_nccl.CommInitRank(&ctx->comm, ctx->world, id, ctx->rank));
-      if (g_nccl.CommSplit) NCCL_CHECK(g_nccl.CommSplit(ctx->comm, 0, ctx->rank, &ctx->comm2, nullptr));
+      // the side-stream communicator is an optimisation: without it (an NCCL that cannot split)
+      // the early-posted halos fall back to the main stream
+      if (g_nccl.CommSplit &&
+          g_nccl.CommSplit(ctx->comm, 0, ctx->rank, &ctx->comm2, nullptr) != ncclSuccess)
+        ctx->comm2 = nullptr;
     }
     CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
     *out = ctx.release();
