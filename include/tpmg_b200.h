@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define TPMG_ABI_VERSION 1
+#define TPMG_ABI_VERSION 2
 
 typedef enum tpmg_status {
   TPMG_OK = 0,
@@ -129,6 +129,16 @@ typedef struct tpmg_mg_config {
   int nu_pre;       /* sweeps on refined levels; coarsest is forced to 1+0 (multigrid.hpp:269-270) */
   int nu_post;
   int depth;        /* number of levels; 0 = coarsen while every tile dim stays even and >= 2 */
+  /* Coarse-grid agglomeration of a decomposed run (world > 1, or the loopback test mode): every
+   * level whose GLOBAL grid has at most `agglomerate` columns is kept whole on every rank and
+   * the bottom of the V-cycle is solved redundantly there -- the restricted right-hand side is
+   * all-gathered once per V-cycle (NCCL all-gather, or each rank's tile stored straight into
+   * every rank's copy through CUDA-IPC peer mappings) and each rank prolongates from its copy.
+   * The levels are then those of the GLOBAL grid (depth 0: coarsen it while it stays even and
+   * >= 4 per dimension), so the solve is bitwise the one-rank solve of the same problem and
+   * the coarse grid does not grow with the rank count.  0 = off (every level decomposed, the
+   * reference's one-coarse-cell-per-process layout).  Ignored on one rank. */
+  int agglomerate;
 } tpmg_mg_config;
 
 /* ---- context ------------------------------------------------------------------------------ */

@@ -119,7 +119,7 @@ class ProfileGrid(C.Structure):  # tpmg_profile_grid
 class MGConfig(C.Structure):
     _fields_ = [("smoother", C.c_int), ("relax", C.c_double), ("prolongation", C.c_int),
                 ("restriction", C.c_int), ("nu_pre", C.c_int), ("nu_post", C.c_int),
-                ("depth", C.c_int)]
+                ("depth", C.c_int), ("agglomerate", C.c_int)]
 
 
 _libs: dict = {}

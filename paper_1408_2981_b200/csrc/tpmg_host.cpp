@@ -110,7 +110,7 @@ thread_local std::string g_global_error;
 // in that segment around stream synchronisations: no kernel ever waits on another rank.
 constexpr int kIpcMaxRanks = 64, kIpcMaxLevels = 24;
 constexpr int kIpcGatherMax = 32768;  // tile partials per rank (tiles up to 2048 x 2048 columns)
-constexpr uint64_t kIpcMagic = 0x31637069676d7074ull;  // "tpmgipc1"
+constexpr uint64_t kIpcMagic = 0x32637069676d7074ull;  // "tpmgipc2"
 struct IpcShm {
   std::atomic<uint64_t> magic;
   std::atomic<uint32_t> count, gen, abort;
@@ -118,6 +118,7 @@ struct IpcShm {
   double vals[2][kIpcMaxRanks];  // per-rank contributions, alternating phases
   double gather[2][kIpcMaxRanks][kIpcGatherMax];  // per-rank tile partials, alternating phases
   cudaIpcMemHandle_t handles[kIpcMaxRanks][kIpcMaxLevels][3];  // receive buffers per level / set
+  cudaIpcMemHandle_t agg[kIpcMaxRanks];  // each rank's replicated copy of the agglomerated level's f
 };
 static_assert(std::atomic<uint32_t>::is_always_lock_free, "process-shared atomics");
 
@@ -174,6 +175,9 @@ struct DevBufT {
 using DevBuf = DevBufT<double>;
 
 struct Level {
+  // replicated (coarse-grid agglomeration): the whole global level on every rank, solved
+  // redundantly; nx/ny are the global dims and x0 = y0 = 0
+  bool rep = false;
   int nx = 0, ny = 0;          // local tile
   int gnx = 0, gny = 0;        // global level dims
   int x0 = 0, y0 = 0;          // tile offset (global cell index)
@@ -243,6 +247,13 @@ struct tpmg_hierarchy_s {
   double* pbuf(int i) { return i == 0 ? p.p : p2.p; }
   DevBuf partials, scal;  // reduction partials; scalars s[0..7]
   DevBuf gathered;        // multi-rank: every rank's tile partials (gather_partials)
+  // coarse-grid agglomeration: levels below agg_la are replicated; agg_tile holds this rank's
+  // block of level agg_la-1 (restricted right-hand side on the way down, the prolongation's
+  // coarse block on the way up), agg_gather every rank's block (NCCL all-gather), agg_peers
+  // every rank's copy of level agg_la-1's f (CUDA-IPC)
+  int agg_la = 0;
+  DevBuf agg_tile, agg_gather;
+  tpmg::PeerDst agg_peers{};
   int* d_err = nullptr;
   double* h_scal = nullptr;  // pinned
   // one-rank PCG host loop: per-iteration scalars published into mapped pinned memory by the
@@ -363,6 +374,11 @@ struct tpmg_hierarchy_s {
 bool tpmg_hierarchy_s::multi() const { return ctx->world > 1 || loopback; }
 
 namespace {
+// level l is split over the ranks (halo exchanges); replicated levels behave like one rank
+bool lmulti(tpmg_hierarchy h, int l) { return h->multi() && !h->lv[l].rep; }
+}  // namespace
+
+namespace {
 
 // host barrier of the IPC ranks (sense by generation count); a rank that fails or times out
 // raises the abort flag so the others fail instead of waiting forever
@@ -468,6 +484,36 @@ int plan_levels(int64_t NX, int64_t NY, int px, int py, int depth, bool linear) 
   return levels;
 }
 
+// Coarse-grid agglomeration (tpmg_mg_config::agglomerate > 0 on a decomposed run): the levels
+// are those of the GLOBAL grid; the finest level and every coarser one whose global grid has more
+// than `agg` columns and splits evenly over the process grid stay decomposed, the rest (a prefix
+// of coarse levels) are replicated.  The restriction into the finest replicated level forms
+// each rank's block of it, so that level's dims must split evenly too.  Returns the number of
+// levels; *la = the coarsest decomposed level (0: none replicated).
+int plan_agg(int64_t NX, int64_t NY, int px, int py, int depth, bool linear, int64_t agg, int* la) {
+  const int levels = plan_levels(NX, NY, 1, 1, depth, linear);
+  auto splits = [&](int l) {
+    const int sh = levels - 1 - l;
+    return ((NX >> sh) % px) == 0 && ((NY >> sh) % py) == 0;
+  };
+  if (!splits(levels - 1))
+    throw Error(TPMG_E_CONFIG, "global grid does not split evenly over the process grid");
+  int a = levels - 1;
+  while (a > 0) {
+    const int c = a - 1, sh = levels - 1 - c;
+    if ((NX >> sh) * (NY >> sh) <= agg || !splits(c)) break;
+    a = c;
+  }
+  if (a > 0 && !splits(a - 1)) {
+    if (a == levels - 1)
+      throw Error(TPMG_E_CONFIG,
+                  "agglomeration: the finest tile does not coarsen evenly onto its ranks' blocks");
+    ++a;  // a is decomposed, so its tiles split: the gather lands one level higher
+  }
+  *la = a;
+  return levels;
+}
+
 // ---- halos -----------------------------------------------------------------------------
 // Exchange the 1-cell faces of u on level l with the 4 neighbouring ranks and return the
 // view the kernels read across the tile faces.  Dimensions with a single rank wrap onto the
@@ -478,7 +524,7 @@ Halo halo_view(tpmg_hierarchy h, int l, const double* u, int set) {
   tpmg_context ctx = h->ctx;
   Level& L = h->lv[l];
   Halo H = tpmg::self_halo(u, L.nx, L.ny, L.plane);
-  if (!h->multi()) return H;
+  if (!lmulti(h, l)) return H;
   const bool xs = ctx->px > 1 || h->loopback, ys = ctx->py > 1 || h->loopback;
   const int64_t nwe = (int64_t)L.ny * h->nz, nsn = (int64_t)L.nx * h->nz;
   double* rW = (set ? L.recv2 : L.recv).p;
@@ -498,7 +544,7 @@ Halo exchange(tpmg_hierarchy h, int l, const double* u, int set = 0) {
   Level& L = h->lv[l];
   DevBuf& SB = set ? L.send2 : L.send;
   DevBuf& RB = set ? L.recv2 : L.recv;
-  if (!h->multi()) return tpmg::self_halo(u, L.nx, L.ny, L.plane);
+  if (!lmulti(h, l)) return tpmg::self_halo(u, L.nx, L.ny, L.plane);
   const int nz = h->nz;
   const int64_t nwe = (int64_t)L.ny * nz, nsn = (int64_t)L.nx * nz;
   double* sW = SB.p;
@@ -577,9 +623,9 @@ tpmg::Halo2 exchange_deep(tpmg_hierarchy h, int l, const double* u) {
   tpmg_context ctx = h->ctx;
   Level& L = h->lv[l];
   tpmg::Halo2 H{};
-  H.xs = h->multi() && (ctx->px > 1 || h->loopback);
-  H.ys = h->multi() && (ctx->py > 1 || h->loopback);
-  if (!h->multi()) return H;
+  H.xs = lmulti(h, l) && (ctx->px > 1 || h->loopback);
+  H.ys = lmulti(h, l) && (ctx->py > 1 || h->loopback);
+  if (!lmulti(h, l)) return H;
   const int nz = h->nz;
   int64_t off[8], cnt[8];
   deep_offsets(L, nz, off, cnt);
@@ -805,13 +851,14 @@ void probe_collect(tpmg_hierarchy h) {
 void dot_into(tpmg_hierarchy h, int l, const double* a, const double* b, int slot) {
   Level& L = h->lv[l];
   int nb = 0;
-  if (!h->generic && tpmg::dot_tiles_ok(L.nx, L.ny)) {
-    tpmg::launch_dot_tiles(h->ctx->launch(), L.nx, L.ny, h->nz, a, b, h->partials.p, &nb);
-    finish_dot(h, nb, slot, l);
-  } else {
-    tpmg::launch_dot(h->ctx->launch(), L.plane * h->nz, a, b, h->partials.p, &nb);
-    finish_dot(h, nb, slot);
+  const bool tiles = !h->generic && tpmg::dot_tiles_ok(L.nx, L.ny);
+  if (tiles) tpmg::launch_dot_tiles(h->ctx->launch(), L.nx, L.ny, h->nz, a, b, h->partials.p, &nb);
+  else tpmg::launch_dot(h->ctx->launch(), L.plane * h->nz, a, b, h->partials.p, &nb);
+  if (L.rep) {  // a replicated level is whole on every rank: no sum over the ranks
+    tpmg::launch_reduce(h->ctx->launch(), h->partials.p, nb, h->scal.p + slot);
+    return;
   }
+  finish_dot(h, nb, slot, tiles ? l : -1);
 }
 
 // ---- hot-path building blocks ------------------------------------------------------------
@@ -847,10 +894,53 @@ void sweep(tpmg_hierarchy h, int l, const double* u_in, const double* f, double*
 // fine level lf -> coarse lf-1: coarse = R (f - A u).  `scratch` is a free fine-level buffer.
 void restrict_plain(tpmg_hierarchy h, int lf, const double* fine, double* coarse, int kind);
 
+// ---- coarse-grid agglomeration ---------------------------------------------------------------
+// Every rank's block of the replicated level lc (this rank's in h->agg_tile, formed by the
+// restriction from the decomposed level lc+1) into dst, the whole level, on every rank.
+void agg_gather(tpmg_hierarchy h, int lc, double* dst) {
+  tpmg_context ctx = h->ctx;
+  const Level& F = h->lv[lc + 1];
+  const Level& C = h->lv[lc];
+  const int bnx = F.nx / 2, bny = F.ny / 2, nz = h->nz;
+  const int64_t bn = (int64_t)bnx * bny * nz;
+  if (ctx->ipc) {
+    // the all-gather as NVLink peer stores: this rank's block goes straight into every rank's
+    // copy (between barriers: every copy's readers are done, then every block has landed)
+    CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    ipc_barrier(ctx);
+    tpmg::launch_block_to_peers(ctx->launch(), h->agg_tile.p, bnx, bny, nz, F.x0 / 2, F.y0 / 2,
+                                C.nx, C.ny, h->agg_peers);
+    CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    ipc_barrier(ctx);
+    if (dst != C.f.p)
+      CUDA_CHECK(cudaMemcpyAsync(dst, C.f.p, (size_t)C.plane * nz * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, ctx->stream));
+  } else if (ctx->world > 1) {
+    NCCL_CHECK(g_nccl.AllGather(h->agg_tile.p, h->agg_gather.p, (size_t)bn, ncclDouble, ctx->comm,
+                                ctx->stream));
+    tpmg::launch_blocks_to_level(ctx->launch(), h->agg_gather.p, ctx->px, ctx->py, bnx, bny, nz,
+                                 dst);
+  } else {  // loopback: the one block is the whole level
+    tpmg::launch_blocks_to_level(ctx->launch(), h->agg_tile.p, 1, 1, bnx, bny, nz, dst);
+  }
+}
+// crossing from a decomposed level lf to a replicated level lf-1
+bool agg_boundary(tpmg_hierarchy h, int lf) { return h->lv[lf - 1].rep && !h->lv[lf].rep; }
+
+void resid_restrict_impl(tpmg_hierarchy h, int lf, const double* u, const double* f,
+                         double* coarse, double* scratch, bool probe);
+// fine level lf -> coarse lf-1: coarse = R (f - A u); at the agglomeration boundary the rank's
+// block is formed, then gathered into the replicated level on every rank
 void resid_restrict(tpmg_hierarchy h, int lf, const double* u, const double* f, double* coarse,
                     double* scratch, bool probe = false) {
+  if (!agg_boundary(h, lf)) return resid_restrict_impl(h, lf, u, f, coarse, scratch, probe);
+  resid_restrict_impl(h, lf, u, f, h->agg_tile.p, scratch, probe);
+  agg_gather(h, lf - 1, coarse);
+}
+
+void resid_restrict_impl(tpmg_hierarchy h, int lf, const double* u, const double* f,
+                         double* coarse, double* scratch, bool probe) {
   Level& F = h->lv[lf];
-  Level& C = h->lv[lf - 1];
   // f's face halo posted early by exchange_f_async (joined here whichever path runs)
   const bool f_posted = F.f_pending;
   const Halo hf_posted = f_posted ? finish_f_async(h, lf, f) : Halo{};
@@ -864,7 +954,7 @@ void resid_restrict(tpmg_hierarchy h, int lf, const double* u, const double* f, 
     tpmg::launch_resid_restrict_sum(h->ctx->launch(), h->vcoef(), F.coef(h->nz), h->xi, u, H, f,
                                     coarse);
   } else if (h->fuse_rr && tpmg::resid_restrict_T_fusable(F.coef(h->nz)) &&
-             (!h->multi() || (F.d_ringc.p && tpmg::resid_restrict_T2_fusable(F.coef(h->nz))))) {
+             (!lmulti(h, lf) || (F.d_ringc.p && tpmg::resid_restrict_T2_fusable(F.coef(h->nz))))) {
     // decomposed: u's two-cell halo with corners and f's face halo first (the ring residuals
     // the transpose stencil reaches outside the tile)
     const tpmg::Halo2 hu = exchange_deep(h, lf, u);
@@ -876,24 +966,30 @@ void resid_restrict(tpmg_hierarchy h, int lf, const double* u, const double* f, 
   } else {
     apply_level(h, lf, tpmg::APPLY_RESID, u, f, scratch);
     const Halo Hr = exchange(h, lf, scratch);
-    tpmg::launch_restrict_transpose(h->ctx->launch(), C.nx, C.ny, h->nz, scratch, Hr, coarse);
+    tpmg::launch_restrict_transpose(h->ctx->launch(), F.nx / 2, F.ny / 2, h->nz, scratch, Hr,
+                                    coarse);
   }
 }
 
 void restrict_plain(tpmg_hierarchy h, int lf, const double* fine, double* coarse, int kind = -1) {
   Level& C = h->lv[lf - 1];
+  const Level& F = h->lv[lf];
   if (kind < 0) kind = h->restriction;
   if (h->generic) {
     tpmg::launch_restrict_gen(h->ctx->launch(), C.coef(h->nz), C.d_children.p, h->rule,
                               h->lv[lf].plane, fine, coarse, kind == TPMG_RESTRICT_TRANSPOSE);
     return;
   }
+  // the coarse block of this rank's fine tile (at the agglomeration boundary: gathered after)
+  const bool gather = agg_boundary(h, lf);
+  double* dst = gather ? h->agg_tile.p : coarse;
   if (kind == TPMG_RESTRICT_SUMMATION) {
-    tpmg::launch_restrict_sum(h->ctx->launch(), C.nx, C.ny, h->nz, fine, coarse);
+    tpmg::launch_restrict_sum(h->ctx->launch(), F.nx / 2, F.ny / 2, h->nz, fine, dst);
   } else {
     const Halo Hf = exchange(h, lf, fine);
-    tpmg::launch_restrict_transpose(h->ctx->launch(), C.nx, C.ny, h->nz, fine, Hf, coarse);
+    tpmg::launch_restrict_transpose(h->ctx->launch(), F.nx / 2, F.ny / 2, h->nz, fine, Hf, dst);
   }
+  if (gather) agg_gather(h, lf - 1, coarse);
 }
 
 void prolong_level(tpmg_hierarchy h, int lc, const double* coarse, double* fine, bool add,
@@ -904,6 +1000,20 @@ void prolong_level(tpmg_hierarchy h, int lc, const double* coarse, double* fine,
     Level& C = h->lv[lc];
     tpmg::launch_prolong_gen(h->ctx->launch(), C.coef(h->nz), C.d_children.p, h->rule, F.plane,
                              coarse, fine, linear, add);
+    return;
+  }
+  if (agg_boundary(h, lc + 1)) {
+    // from this rank's block of the replicated coarse level; its halo is read straight from the
+    // replicated copy (periodic views)
+    const Level& C = h->lv[lc];
+    const int bnx = F.nx / 2, bny = F.ny / 2, x0 = F.x0 / 2, y0 = F.y0 / 2;
+    tpmg::launch_block_from_level(h->ctx->launch(), coarse, C.nx, C.ny, h->nz, x0, y0, bnx, bny,
+                                  h->agg_tile.p);
+    const Halo Hc = linear ? tpmg::block_halo(coarse, C.nx, C.ny, C.plane, x0, y0, bnx, bny)
+                           : Halo{};
+    if (probe) probe_begin(h, TPMG_K_PROLONG_ADD);
+    tpmg::launch_prolong(h->ctx->launch(), F.nx, F.ny, h->nz, h->agg_tile.p, Hc, fine, linear, add);
+    if (probe) probe_end(h, TPMG_K_PROLONG_ADD);
     return;
   }
   const Halo Hc = linear ? exchange(h, lc, coarse) : Halo{};
@@ -1484,6 +1594,8 @@ void ipc_connect(tpmg_hierarchy h) {
       const double* b = set == 2 ? h->lv[l].recv3.p : (set ? h->lv[l].recv2.p : h->lv[l].recv.p);
       if (b) CUDA_CHECK(cudaIpcGetMemHandle(&S->handles[ctx->rank][l][set], (void*)b));
     }
+  if (h->agg_la > 0)
+    CUDA_CHECK(cudaIpcGetMemHandle(&S->agg[ctx->rank], (void*)h->lv[h->agg_la - 1].f.p));
   ipc_barrier(ctx);
   std::unordered_map<int64_t, double*> opened;
   auto base = [&](int r, int l, int set) {
@@ -1511,6 +1623,7 @@ void ipc_connect(tpmg_hierarchy h) {
         L.peer[set][3] = base(north, l, set) + 2 * nwe;        // -> north's S segment
       }
     }
+    if (L.rep) continue;
     if (L.recv3.p) {  // deep piece d -> slot kOpp[d] of the neighbour in direction d
       int64_t off[8], cnt[8];
       deep_offsets(L, h->nz, off, cnt);
@@ -1518,6 +1631,19 @@ void ipc_connect(tpmg_hierarchy h) {
         if (deep_live(h, d))
           L.peer3[d] = base(ctx->rank_of(ctx->rx + kDeepDx[d], ctx->ry + kDeepDy[d]), l, 2) +
                        off[kOpp[d]];
+    }
+  }
+  if (h->agg_la > 0) {  // every rank's copy of the finest replicated level's f (own included)
+    h->agg_peers.n = ctx->world;
+    for (int r = 0; r < ctx->world; ++r) {
+      if (r == ctx->rank) {
+        h->agg_peers.p[r] = h->lv[h->agg_la - 1].f.p;
+        continue;
+      }
+      void* p = nullptr;
+      CUDA_CHECK(cudaIpcOpenMemHandle(&p, S->agg[r], cudaIpcMemLazyEnablePeerAccess));
+      h->ipc_mapped.push_back(p);
+      h->agg_peers.p[r] = static_cast<double*>(p);
     }
   }
   ipc_barrier(ctx);
@@ -1574,16 +1700,21 @@ int hier_create_impl(tpmg_context ctx, const tpmg_grid_desc* g, const tpmg_facto
       if (fp->xi_r) check_finite(fp->xi_r, (nz + 1) * ncf, "xi_r");
     }
 
-    const int levels = plan_levels(NX, NY, ctx->px, ctx->py, cfg->depth,
-                                   cfg->prolongation == TPMG_PROLONG_LINEAR ||
-                                       cfg->restriction == TPMG_RESTRICT_TRANSPOSE);
-
+    if (cfg->agglomerate < 0) throw Error(TPMG_E_CONFIG, "negative agglomeration threshold");
+    const bool linear_tr = cfg->prolongation == TPMG_PROLONG_LINEAR ||
+                           cfg->restriction == TPMG_RESTRICT_TRANSPOSE;
     auto h = std::make_unique<tpmg_hierarchy_s>();
     h->ctx = ctx;
     {
       const char* e = getenv("TPMG_LOOPBACK");
       h->loopback = ctx->world == 1 && e && atoi(e) != 0;
     }
+    const bool agg = h->multi() && cfg->agglomerate > 0;
+    if (agg && ctx->world > kIpcMaxRanks && ctx->ipc)
+      throw Error(TPMG_E_CONFIG, "agglomeration: too many ranks for the IPC transport");
+    const int levels =
+        agg ? plan_agg(NX, NY, ctx->px, ctx->py, cfg->depth, linear_tr, cfg->agglomerate, &h->agg_la)
+            : plan_levels(NX, NY, ctx->px, ctx->py, cfg->depth, linear_tr);
     h->nz = (int)nz;
     h->xi = fp ? fp->xi_r != nullptr : (p->xi_r_r != nullptr && p->xi_r_s != nullptr);
     h->cm = cm;
@@ -1645,9 +1776,11 @@ int hier_create_impl(tpmg_context ctx, const tpmg_grid_desc* g, const tpmg_facto
     double hx = g->hx, hy = g->hy;
     for (int l = levels - 1; l >= 0; --l) {
       Level& L = h->lv[l];
+      L.rep = l < h->agg_la;  // replicated: the whole global level on this rank
+      const int lpx = L.rep ? 1 : ctx->px, lpy = L.rep ? 1 : ctx->py;
       L.gnx = (int)gx; L.gny = (int)gy;
-      L.nx = (int)(gx / ctx->px); L.ny = (int)(gy / ctx->py);
-      L.x0 = ctx->rx * L.nx; L.y0 = ctx->ry * L.ny;
+      L.nx = (int)(gx / lpx); L.ny = (int)(gy / lpy);
+      L.x0 = L.rep ? 0 : ctx->rx * L.nx; L.y0 = L.rep ? 0 : ctx->ry * L.ny;
       L.plane = (int64_t)L.nx * L.ny;
       const int64_t gnc = gx * gy;
       // assemble_hatted (factorised), discretization.hpp:256-274, flat Cartesian geometry
@@ -1678,7 +1811,7 @@ int hier_create_impl(tpmg_context ctx, const tpmg_grid_desc* g, const tpmg_facto
       L.d_ss.upload(ss.data(), L.plane);
       L.d_sn.upload(sn.data(), L.plane);
       L.cm = cm;
-      if (h->multi() && cm == tpmg::CM_FACT && l > 0) {
+      if (h->multi() && !L.rep && cm == tpmg::CM_FACT && l > 0) {
         // the same scalars on the 1-cell ring around the tile (tpmg::kRingFields layout), for the
         // ring residuals of the decomposed fused residual + transpose restriction
         const int64_t rn = 2 * (int64_t)L.ny + 2 * (int64_t)L.nx;
@@ -1829,7 +1962,7 @@ int hier_create_impl(tpmg_context ctx, const tpmg_grid_desc* g, const tpmg_facto
         L.u.alloc(n);
         L.f.alloc(n);
       }
-      if (h->multi()) {
+      if (h->multi() && !L.rep) {
         const int64_t faces = 2 * (int64_t)L.ny * nz + 2 * (int64_t)L.nx * nz;
         L.send.alloc(faces);
         L.recv.alloc(faces);
@@ -1848,6 +1981,12 @@ int hier_create_impl(tpmg_context ctx, const tpmg_grid_desc* g, const tpmg_facto
       // one partial per 256-column block (k_apply) or per 32x4 tile (k_apply_tiled)
       max_blocks = std::max<int64_t>(max_blocks, (L.plane + 255) / 256 + 1);
       max_blocks = std::max<int64_t>(max_blocks, L.plane / 128 + 1);
+    }
+    if (h->agg_la > 0) {  // this rank's block of the finest replicated level (+ all ranks')
+      const Level& A = h->lv[h->agg_la];
+      const int64_t bn = (int64_t)(A.nx / 2) * (A.ny / 2) * nz;
+      h->agg_tile.alloc(bn);
+      if (ctx->world > 1 && !ctx->ipc) h->agg_gather.alloc((size_t)ctx->world * bn);
     }
     const int64_t nf = h->lv[levels - 1].plane * nz;
     h->r.alloc(nf); h->z.alloc(nf); h->p.alloc(nf); h->q.alloc(nf); h->tmp.alloc(nf);

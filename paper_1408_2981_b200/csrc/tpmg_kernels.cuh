@@ -275,4 +275,27 @@ void launch_pack_faces(const Launch& L, int nx, int ny, int nz, const double* u,
 // The two-cell faces and 2x2 corners of u (Halo2 layouts of the receiving ranks) written to dst.
 void launch_pack_deep(const Launch& L, int nx, int ny, int nz, const double* u, const DeepDst& dst);
 
+// ---- coarse-grid agglomeration (tpmg_mg_config::agglomerate) ---------------------------------
+// A replicated level is held whole ([k][gny][gnx]) on every rank; the ranks' blocks of it are
+// bnx x bny (rank r = ry*px + rx owns the block at (rx*bnx, ry*bny)).
+constexpr int kMaxPeers = 64;
+struct PeerDst {
+  double* p[kMaxPeers];  // every rank's replicated copy (CUDA-IPC mappings; own copy included)
+  int n;
+};
+// dst[k][y][x] = the blocks of all ranks, gathered [r][k][j][i] (NCCL all-gather; px = py = 1:
+// one block, the loopback identity)
+void launch_blocks_to_level(const Launch& L, const double* gathered, int px, int py, int bnx,
+                            int bny, int nz, double* dst);
+// this rank's block (bnx x bny at x0, y0) stored into every rank's replicated copy (NVLink peer
+// stores): the all-gather of the CUDA-IPC transport
+void launch_block_to_peers(const Launch& L, const double* blk, int bnx, int bny, int nz, int x0,
+                           int y0, int gnx, int gny, const PeerDst& dst);
+// blk[k][j][i] = src[k][y0+j][x0+i] of a replicated level (the rank's block, for the prolongation)
+void launch_block_from_level(const Launch& L, const double* src, int gnx, int gny, int nz, int x0,
+                             int y0, int bnx, int bny, double* blk);
+// the face halo of the block at (x0, y0) as strided views into the replicated level (periodic)
+Halo block_halo(const double* src, int gnx, int gny, int64_t gplane, int x0, int y0, int bnx,
+                int bny);
+
 }  // namespace tpmg

@@ -194,6 +194,7 @@ class Problem:
     nu_pre: int = 1
     nu_post: int = 1
     depth: int = 0
+    agglomerate: int = 0  # global column count at or below which a decomposed run replicates levels
     tol: float = 1e-8
     rhs_seed: int = 0
     name: str = ""
@@ -215,7 +216,7 @@ class Problem:
     def mg_kwargs(self) -> dict:
         return dict(relax=self.relax, prolongation=self.prolongation,
                     restriction=self.restriction, nu_pre=self.nu_pre, nu_post=self.nu_post,
-                    depth=self.depth)
+                    depth=self.depth, agglomerate=self.agglomerate)
 
 
 def edge_profile(h: np.ndarray, nx: int, ny: int) -> np.ndarray:

@@ -238,7 +238,7 @@ class Hierarchy:
             self._keep += [xr, xs]
         prof = FactorizedProfiles(_p(br), _p(asr), _p(arr), _p(xr), _p(bs), _p(ars), _p(xs), _p(ass))
         cfg = MGConfig(kw.get("smoother", 0), kw["relax"], kw["prolongation"], kw["restriction"],
-                       kw["nu_pre"], kw["nu_post"], kw["depth"])
+                       kw["nu_pre"], kw["nu_post"], kw["depth"], kw.get("agglomerate", 0))
         h = C.c_void_p()
         self._h = None
         coef = getattr(P, "coef", "factorized")

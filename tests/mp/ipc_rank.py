@@ -14,6 +14,11 @@ import numpy as np  # noqa: E402
 
 from paper_1408_2981_b200 import synth, tpmg  # noqa: E402
 
+def _agg(P, cols):
+    P.agglomerate = cols
+    return P
+
+
 PROBLEMS = {
     "cfg1": lambda: synth.baseline_config(1),
     # 32x4-tiled kernels and the TMA pipelines on every rank's finest tiles
@@ -25,6 +30,14 @@ PROBLEMS = {
     "rr2": lambda: synth.make_problem(256, 128, 16, omega2=1e-2, lambda2=1e-4,
                                       grading="geometric", ratio=1.2, profile="lognormal",
                                       profile_seed=6, profile_sigma=0.5, depth=4, name="rr2"),
+    # coarse-grid agglomeration: levels of <= 512 global columns replicated on every rank
+    "tiled_agg": lambda: _agg(synth.make_problem(128, 64, 16, omega2=1e-2, lambda2=1e-4,
+                                                 grading="quadratic", profile="uniform",
+                                                 profile_seed=3, depth=4, name="tiled-agg"), 512),
+    "rr2_agg": lambda: _agg(synth.make_problem(256, 128, 16, omega2=1e-2, lambda2=1e-4,
+                                               grading="geometric", ratio=1.2, profile="lognormal",
+                                               profile_seed=6, profile_sigma=0.5, depth=5,
+                                               name="rr2-agg"), 2048),
     "cfg5s": lambda: synth.make_problem(64, 64, 16, omega2=1e-5, lambda2=1e-6,
                                         grading="geometric", ratio=1.1, profile="lognormal",
                                         profile_seed=2, depth=4, nu=2, tol=1e-10, name="cfg5-small"),

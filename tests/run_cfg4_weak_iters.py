@@ -5,10 +5,13 @@ dots reduce in the one-rank tile order, tests/test_ipc_multirank.py), so the ite
 printed here are those of the 1/2/4/8-GPU runs: they show how the convergence responds to the
 growing global coarse grid (8x8 per GPU).  Validation driver, not a pytest file.
 
-    python tests/run_cfg4_weak_iters.py [max_gpus] [--global]
+    python tests/run_cfg4_weak_iters.py [max_gpus] [--coarsening=tile|global|agglomerate]
 
---global: coarsen the global grid as deep as the decomposition allows (depth 0: tiles of 2x2 at
-the bottom) instead of BASELINE's 8x8 per GPU tile.
+tile (default here, BASELINE's literal reading): 8 levels per GPU tile, the global coarse grid
+grows with N; global: every level decomposed, coarsened as deep as the decomposition allows
+(depth 0); agglomerate (bench.py's multi-GPU default): the global grid coarsened to 8 cells along
+its longer side, levels of <= 128^2 columns replicated on every GPU -- bitwise the one-rank
+solve of the same global problem, so these one-GPU runs give its iteration counts exactly.
 """
 import os
 import sys
@@ -27,15 +30,18 @@ import bench  # noqa: E402  (the problem definition bench.py --config 4w uses)
 def main():
     args = [a for a in sys.argv[1:] if not a.startswith("--")]
     top = int(args[0]) if args else 8
-    deep = "--global" in sys.argv
+    mode = "tile"
+    for a in sys.argv[1:]:
+        if a.startswith("--coarsening="):
+            mode = a.split("=", 1)[1]
+        elif a == "--global":
+            mode = "global"
     ctx = tpmg.Context()
     for n in (1, 2, 4, 8):
         if n > top:
             break
         px, py = bench.proc_grid(n)
-        P, workload, _, _ = bench.make_problem("4w", px, py)
-        if deep:
-            P.depth = 0
+        P, workload, _, _ = bench.make_problem("4w", px, py, mode)
         h = tpmg.Hierarchy(ctx, P)
         f = h.field().upload(P.rhs())
         x = h.field()

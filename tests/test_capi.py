@@ -35,7 +35,7 @@ def test_library_exports_every_declared_symbol(variant):
     missing = [f for f in header_functions() if not hasattr(lib, f)]
     assert not missing, missing
     L = _capi.load(variant)
-    assert L.tpmg_abi_version() == 1
+    assert L.tpmg_abi_version() == 2
     assert L.tpmg_status_string(0) == b"ok"
     assert L.tpmg_status_string(5) == b"singular_error"
 

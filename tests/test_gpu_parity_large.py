@@ -82,15 +82,19 @@ def test_pcg_host_entry_k_fastest_matches_golden(gpu_ctx, name):
         h.close()
 
 
+@pytest.mark.parametrize("agg", [0, 128 * 128])
 @pytest.mark.parametrize("name", ["cfg3", "cfg5t"])
-def test_decomposed_paths_match_golden_at_baseline_size(gpu_ctx, monkeypatch, name):
+def test_decomposed_paths_match_golden_at_baseline_size(gpu_ctx, monkeypatch, name, agg):
     """The multi-rank device paths at BASELINE's sizes (TPMG_LOOPBACK=1: the rank is its own
     periodic neighbour, so every face and two-cell halo is packed into receive buffers and read
     back from them, the decomposed fused residual + restriction reads the coefficient ring, and
     the multi-rank schedule runs) reproduce the one-rank oracle golden bit for bit -- the
-    decomposed code computes the reference's numbers, not just close ones."""
+    decomposed code computes the reference's numbers, not just close ones.  agg > 0: coarse-grid
+    agglomeration, levels of <= 128^2 columns replicated (restricted block gathered into the
+    replicated level, the prolongation from the rank's block of it with halo views)."""
     g = _golden(name)
     P = synth.parity_problem(name)
+    P.agglomerate = agg
     monkeypatch.setenv("TPMG_LOOPBACK", "1")
     h = tpmg.Hierarchy(gpu_ctx, P)
     try:

@@ -59,7 +59,7 @@ def assemble(parts, key, P):
     return g
 
 
-@pytest.mark.parametrize("name", ["cfg1", "tiled", "cfg5s", "rr2"])
+@pytest.mark.parametrize("name", ["cfg1", "tiled", "cfg5s", "rr2", "tiled_agg", "rr2_agg"])
 @pytest.mark.parametrize("grid", [(2, 1), (1, 2), (2, 2)])
 def test_ipc_ranks_match_global_oracle(tmp_path, oracle_mod, name, grid):
     px, py = grid
