@@ -348,6 +348,9 @@ const char* tpmg_profile_last_error(void);
 /* ---- instrumentation ------------------------------------------------------------------------ */
 /* Number of kernels this library launched on the context since creation. */
 int tpmg_kernel_launch_count(tpmg_context ctx, int64_t* out);
+/* NCCL API calls (sends, receives, collectives, group brackets; captured ones counted at capture)
+ * this process has issued: 0 on a one-rank context, whose halos are periodic self views. */
+int tpmg_nccl_call_count(int64_t* out);
 /* Kernel ids for tpmg_time_kernel. */
 typedef enum tpmg_kernel_id {
   TPMG_K_APPLY = 0,           /* y = A u                                  */

@@ -76,6 +76,7 @@ SIGNATURES = {
     "tpmg_pcg_host": (C.c_int, [_VP, _D, _D, C.c_int, C.c_double, C.c_int, _D, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "tpmg_pcg_host_batch": (C.c_int, [_VP, C.c_int, C.POINTER(_D), C.POINTER(_D), C.c_int, C.c_double, C.c_int, _D, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "tpmg_kernel_launch_count": (C.c_int, [_VP, C.POINTER(C.c_int64)]),
+    "tpmg_nccl_call_count": (C.c_int, [C.POINTER(C.c_int64)]),
     "tpmg_set_use_graphs": (C.c_int, [_VP, C.c_int]),
     "tpmg_time_kernel": (C.c_int, [_VP, C.c_int, C.c_int, C.c_int, _D]),
     "tpmg_kernel_probe": (C.c_int, [_VP, C.c_int]),

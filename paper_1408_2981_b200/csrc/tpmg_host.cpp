@@ -94,8 +94,10 @@ struct Nccl {
 };
 Nccl g_nccl;
 
+std::atomic<int64_t> g_nccl_calls{0};  // NCCL API calls issued by this process (tpmg_nccl_call_count)
 #define NCCL_CHECK(x)                                                                   \
   do {                                                                                  \
+    g_nccl_calls.fetch_add(1, std::memory_order_relaxed);                               \
     ncclResult_t r_ = (x);                                                              \
     if (r_ != ncclSuccess)                                                              \
       throw Error(TPMG_E_NCCL, std::string(#x ": ") + g_nccl.GetErrorString(r_));       \
@@ -134,6 +136,9 @@ struct tpmg_context_s {
   // communicator so that its NCCL operations never interleave with the main stream's
   cudaStream_t side = nullptr;
   ncclComm_t comm2 = nullptr;
+  // TPMG_LOOPBACK=2 at tpmg_init, one rank: a one-rank NCCL communicator, so that the loopback
+  // halos and reductions go through the NCCL transport itself (send / receive to self)
+  bool nccl_self = false;
   tpmg::Launch side_launch() { return tpmg::Launch{side, &launches}; }
   // CUDA-IPC transport (tpmg_init_ipc): shared segment, reduction phase, pinned staging
   IpcShm* ipc = nullptr;
@@ -278,6 +283,8 @@ struct tpmg_hierarchy_s {
   // so the GPU parity tests cover it; only the NCCL transport itself is left out
   bool loopback = false;
   bool multi() const;
+  bool nccl_self() const;
+  bool nccl_reduce() const;
   bool pcg_fused = false;  // PCG vector work fused into the finest-level smoother sweeps
   const double* f_first = nullptr;  // fused PCG: the right-hand side the first iteration reads
   bool fuse_rr = true;     // fused residual + transpose restriction (TPMG_FUSE_RR=0 disables)
@@ -372,6 +379,11 @@ struct tpmg_hierarchy_s {
 };
 
 bool tpmg_hierarchy_s::multi() const { return ctx->world > 1 || loopback; }
+// loopback halos carried by NCCL itself (a one-rank communicator): every send / receive of the
+// NCCL transport, its all-gathers and all-reduces run on one GPU, inside the captured graphs too
+bool tpmg_hierarchy_s::nccl_self() const { return loopback && ctx->nccl_self; }
+// the rank's reductions go over NCCL
+bool tpmg_hierarchy_s::nccl_reduce() const { return !ctx->ipc && (ctx->world > 1 || nccl_self()); }
 
 namespace {
 // level l is split over the ranks (halo exchanges); replicated levels behave like one rank
@@ -568,21 +580,22 @@ Halo exchange(tpmg_hierarchy h, int l, const double* u, int set = 0) {
     tpmg::launch_pack_faces(ctx->launch(), L.nx, L.ny, nz, u, dst);
     CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
     ipc_barrier(ctx);
-  } else if (h->loopback) {  // this rank is its own neighbour on every side
+  } else if (h->loopback && !h->nccl_self()) {  // this rank is its own neighbour on every side
     tpmg::launch_pack_faces(ctx->launch(), L.nx, L.ny, nz, u, tpmg::FaceDst{{rE, rW, rN, rS}});
   } else {
+  const bool xs = ctx->px > 1 || h->loopback, ys = ctx->py > 1 || h->loopback;
   tpmg::launch_pack_faces(ctx->launch(), L.nx, L.ny, nz, u,
-                          tpmg::FaceDst{{ctx->px > 1 ? sW : nullptr, ctx->px > 1 ? sE : nullptr,
-                                         ctx->py > 1 ? sS : nullptr, ctx->py > 1 ? sN : nullptr}});
+                          tpmg::FaceDst{{xs ? sW : nullptr, xs ? sE : nullptr,
+                                         ys ? sS : nullptr, ys ? sN : nullptr}});
   NCCL_CHECK(g_nccl.GroupStart());
-  if (ctx->px > 1) {
+  if (xs) {
     const int west = ctx->rank_of(ctx->rx - 1, ctx->ry), east = ctx->rank_of(ctx->rx + 1, ctx->ry);
     NCCL_CHECK(g_nccl.Send(sW, nwe, ncclDouble, west, ctx->comm, ctx->stream));
     NCCL_CHECK(g_nccl.Send(sE, nwe, ncclDouble, east, ctx->comm, ctx->stream));
     NCCL_CHECK(g_nccl.Recv(rE, nwe, ncclDouble, east, ctx->comm, ctx->stream));
     NCCL_CHECK(g_nccl.Recv(rW, nwe, ncclDouble, west, ctx->comm, ctx->stream));
   }
-  if (ctx->py > 1) {
+  if (ys) {
     const int south = ctx->rank_of(ctx->rx, ctx->ry - 1), north = ctx->rank_of(ctx->rx, ctx->ry + 1);
     NCCL_CHECK(g_nccl.Send(sS, nsn, ncclDouble, south, ctx->comm, ctx->stream));
     NCCL_CHECK(g_nccl.Send(sN, nsn, ncclDouble, north, ctx->comm, ctx->stream));
@@ -638,7 +651,7 @@ tpmg::Halo2 exchange_deep(tpmg_hierarchy h, int l, const double* u) {
     tpmg::launch_pack_deep(ctx->launch(), L.nx, L.ny, nz, u, dst);
     CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
     ipc_barrier(ctx);
-  } else if (h->loopback) {  // every neighbour is this rank: piece d lands in slot kOpp[d]
+  } else if (h->loopback && !h->nccl_self()) {  // every neighbour is this rank: piece d lands in slot kOpp[d]
     for (int d = 0; d < 8; ++d) dst.p[d] = L.recv3.p + off[kOpp[d]];
     tpmg::launch_pack_deep(ctx->launch(), L.nx, L.ny, nz, u, dst);
   } else {
@@ -673,7 +686,7 @@ tpmg::Halo2 exchange_deep(tpmg_hierarchy h, int l, const double* u) {
 bool f_async_ok(tpmg_hierarchy h) {
   tpmg_context ctx = h->ctx;
   if (!h->multi() || ctx->ipc || !ctx->side) return false;
-  return h->loopback || ctx->comm2;
+  return (h->loopback && !h->nccl_self()) || ctx->comm2;
 }
 
 void exchange_f_async(tpmg_hierarchy h, int l, const double* f) {
@@ -700,21 +713,22 @@ void exchange_f_async(tpmg_hierarchy h, int l, const double* f) {
   double* rN = rS + nsn;
   CUDA_CHECK(cudaEventRecord(h->ev_fsrc[l], ctx->stream));
   CUDA_CHECK(cudaStreamWaitEvent(ctx->side, h->ev_fsrc[l], 0));
-  if (h->loopback) {
+  if (h->loopback && !h->nccl_self()) {
     tpmg::launch_pack_faces(ctx->side_launch(), L.nx, L.ny, nz, f, tpmg::FaceDst{{rE, rW, rN, rS}});
   } else {
+    const bool xs = ctx->px > 1 || h->loopback, ys = ctx->py > 1 || h->loopback;
     tpmg::launch_pack_faces(ctx->side_launch(), L.nx, L.ny, nz, f,
-                            tpmg::FaceDst{{ctx->px > 1 ? sW : nullptr, ctx->px > 1 ? sE : nullptr,
-                                           ctx->py > 1 ? sS : nullptr, ctx->py > 1 ? sN : nullptr}});
+                            tpmg::FaceDst{{xs ? sW : nullptr, xs ? sE : nullptr,
+                                           ys ? sS : nullptr, ys ? sN : nullptr}});
     NCCL_CHECK(g_nccl.GroupStart());
-    if (ctx->px > 1) {
+    if (xs) {
       const int west = ctx->rank_of(ctx->rx - 1, ctx->ry), east = ctx->rank_of(ctx->rx + 1, ctx->ry);
       NCCL_CHECK(g_nccl.Send(sW, nwe, ncclDouble, west, ctx->comm2, ctx->side));
       NCCL_CHECK(g_nccl.Send(sE, nwe, ncclDouble, east, ctx->comm2, ctx->side));
       NCCL_CHECK(g_nccl.Recv(rE, nwe, ncclDouble, east, ctx->comm2, ctx->side));
       NCCL_CHECK(g_nccl.Recv(rW, nwe, ncclDouble, west, ctx->comm2, ctx->side));
     }
-    if (ctx->py > 1) {
+    if (ys) {
       const int south = ctx->rank_of(ctx->rx, ctx->ry - 1), north = ctx->rank_of(ctx->rx, ctx->ry + 1);
       NCCL_CHECK(g_nccl.Send(sS, nsn, ncclDouble, south, ctx->comm2, ctx->side));
       NCCL_CHECK(g_nccl.Send(sN, nsn, ncclDouble, north, ctx->comm2, ctx->side));
@@ -781,7 +795,7 @@ void gather_partials(tpmg_hierarchy h, int nb) {
 // number of ranks.  Other layouts: local fixed-order sum, then a sum over the ranks.
 void finish_dot(tpmg_hierarchy h, int nblocks, int slot, int tile_level = -1) {
   tpmg_context ctx = h->ctx;
-  if (ctx->world > 1 && tile_level >= 0) {
+  if ((ctx->world > 1 || h->nccl_self()) && tile_level >= 0) {
     const Level& L = h->lv[tile_level];
     if (tpmg::dot_tiles_ok(L.nx, L.ny) && nblocks == (L.nx / 32) * (L.ny / 4)) {
       gather_partials(h, nblocks);
@@ -803,7 +817,7 @@ void finish_dot(tpmg_hierarchy h, int nblocks, int slot, int tile_level = -1) {
     CUDA_CHECK(cudaMemcpyAsync(h->scal.p + slot, ctx->ipc_host + 1, sizeof(double),
                                cudaMemcpyHostToDevice, ctx->stream));
     CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
-  } else if (ctx->world > 1) {
+  } else if (h->nccl_reduce()) {
     NCCL_CHECK(g_nccl.AllReduce(h->scal.p + slot, h->scal.p + slot, 1, ncclDouble, ncclSum,
                                 ctx->comm, ctx->stream));
   }
@@ -915,7 +929,7 @@ void agg_gather(tpmg_hierarchy h, int lc, double* dst) {
     if (dst != C.f.p)
       CUDA_CHECK(cudaMemcpyAsync(dst, C.f.p, (size_t)C.plane * nz * sizeof(double),
                                  cudaMemcpyDeviceToDevice, ctx->stream));
-  } else if (ctx->world > 1) {
+  } else if (h->nccl_reduce()) {
     NCCL_CHECK(g_nccl.AllGather(h->agg_tile.p, h->agg_gather.p, (size_t)bn, ncclDouble, ctx->comm,
                                 ctx->stream));
     tpmg::launch_blocks_to_level(ctx->launch(), h->agg_gather.p, ctx->px, ctx->py, bnx, bny, nz,
@@ -1116,7 +1130,7 @@ int sync_err(tpmg_hierarchy h) {
     const int any = (int)ipc_allreduce(h->ctx, (double)e, true);
     CUDA_CHECK(cudaMemcpyAsync(h->d_err, &any, sizeof(int), cudaMemcpyHostToDevice, h->ctx->stream));
     CUDA_CHECK(cudaStreamSynchronize(h->ctx->stream));
-  } else if (h->ctx->world > 1) {
+  } else if (h->nccl_reduce()) {
     NCCL_CHECK(g_nccl.AllReduce(h->d_err, h->d_err, 1, ncclInt32, ncclMax, h->ctx->comm,
                                 h->ctx->stream));
   }
@@ -1450,11 +1464,17 @@ int tpmg_init(const tpmg_context_params* prm, tpmg_context* out) {
     ctx->ry = prm->rank / prm->px;
     CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     tpmg::init_device_constants(ctx->stream);
-    if (ctx->world > 1) {
-      if (!prm->nccl_id) throw Error(TPMG_E_CONFIG, "world_size > 1 needs an ncclUniqueId");
+    {
+      const char* e = getenv("TPMG_LOOPBACK");
+      ctx->nccl_self = ctx->world == 1 && e && atoi(e) == 2;
+    }
+    if (ctx->world > 1 || ctx->nccl_self) {
+      if (!prm->nccl_id && !ctx->nccl_self)
+        throw Error(TPMG_E_CONFIG, "world_size > 1 needs an ncclUniqueId");
       g_nccl.load();
       ncclUniqueId id;
-      std::memcpy(&id, prm->nccl_id, sizeof(id));
+      if (prm->nccl_id) std::memcpy(&id, prm->nccl_id, sizeof(id));
+      else NCCL_CHECK(g_nccl.GetUniqueId(&id));
       NCCL_CHECK(g_nccl.CommInitRank(&ctx->comm, ctx->world, id, ctx->rank));
       // the side-stream communicator is an optimisation: without it (an NCCL that cannot split)
       // the early-posted halos fall back to the main stream
@@ -1986,12 +2006,12 @@ int hier_create_impl(tpmg_context ctx, const tpmg_grid_desc* g, const tpmg_facto
       const Level& A = h->lv[h->agg_la];
       const int64_t bn = (int64_t)(A.nx / 2) * (A.ny / 2) * nz;
       h->agg_tile.alloc(bn);
-      if (ctx->world > 1 && !ctx->ipc) h->agg_gather.alloc((size_t)ctx->world * bn);
+      if (h->nccl_reduce()) h->agg_gather.alloc((size_t)ctx->world * bn);
     }
     const int64_t nf = h->lv[levels - 1].plane * nz;
     h->r.alloc(nf); h->z.alloc(nf); h->p.alloc(nf); h->q.alloc(nf); h->tmp.alloc(nf);
     h->partials.alloc(std::max<int64_t>(max_blocks, 148 * 8));
-    if (ctx->world > 1)  // tile partials of the finest level, every rank's
+    if (ctx->world > 1 || h->nccl_self())  // tile partials of the finest level, every rank's
       h->gathered.alloc((size_t)ctx->world * (h->lv[levels - 1].plane / 128 + 1));
     h->scal.alloc(8);
     CUDA_CHECK(cudaMemsetAsync(h->scal.p, 0, 8 * sizeof(double), h->ctx->stream));
@@ -2855,6 +2875,12 @@ int tpmg_bicgstab(tpmg_hierarchy h, tpmg_field f, tpmg_field x, double tol, int 
 int tpmg_solver_counts(tpmg_hierarchy h, int64_t* n_precond, int64_t* n_matvec) {
   *n_precond = h->n_precond;
   *n_matvec = h->n_matvec;
+  return TPMG_OK;
+}
+
+int tpmg_nccl_call_count(int64_t* out) {
+  if (!out) return TPMG_E_CONFIG;
+  *out = g_nccl_calls.load(std::memory_order_relaxed);
   return TPMG_OK;
 }
 

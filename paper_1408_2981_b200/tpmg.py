@@ -124,6 +124,12 @@ class Context:
         self.lib.tpmg_kernel_launch_count(self._h, C.byref(n))
         return n.value
 
+    def nccl_calls(self) -> int:
+        """NCCL API calls issued by this process so far (0 unless a transport uses NCCL)."""
+        n = C.c_int64()
+        self.lib.tpmg_nccl_call_count(C.byref(n))
+        return n.value
+
     # Handles are freed parent-last whatever order the garbage collector finalises them in
     # (objects in a reference cycle, e.g. held by a traceback, are finalised in arbitrary
     # order): a parent closed while children are alive only marks itself, and the last child
