@@ -280,7 +280,7 @@ struct tpmg_hierarchy_s {
   // face packing, the send -> recv transfer (here device copies onto this rank itself, the
   // periodic neighbour of a 1x1 process grid), kernels reading halos from the recv buffers, the
   // multi-rank schedule (no fused A p / residual+restriction / prolongation) — runs on one GPU,
-  // so the GPU parity tests cover it; only the NCCL transport itself is left out
+  // so the GPU parity tests cover it (TPMG_LOOPBACK=2: with NCCL itself as the transport)
   bool loopback = false;
   bool multi() const;
   bool nccl_self() const;
