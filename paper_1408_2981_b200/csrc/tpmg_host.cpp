@@ -192,6 +192,7 @@ struct Level {
   DevBuf d_bh, d_ah, d_xh, d_sw, d_se, d_ss, d_sn;
   // dense hatted components of the partial / full coefficient modes, [k][y][x]
   int cm = tpmg::CM_FACT;
+  bool uni = false;  // one edge scalar on the whole (global) level: LevelCoef::uni
   DevBuf d_ard, d_bd, d_xid, d_swd, d_sed, d_ssd, d_snd;
   // indirect levels (tpmg_hier_create_generic): neighbour / edge tables, per-edge alpha_s hat,
   // and (coarse levels) the child table on the next finer level
@@ -216,6 +217,7 @@ struct Level {
     c.bh = d_bh.p; c.ah = d_ah.p; c.xh = d_xh.p;
     c.sw = d_sw.p; c.se = d_se.p; c.ss = d_ss.p; c.sn = d_sn.p;
     c.cm = cm;
+    c.uni = uni && cm == tpmg::CM_FACT;
     c.ard = d_ard.p; c.bd = d_bd.p; c.xid = d_xid.p;
     c.swd = d_swd.p; c.sed = d_sed.p; c.ssd = d_ssd.p; c.snd = d_snd.p;
     c.nnb = nnb; c.nbr = d_nbr.p; c.cedge = d_cedge.p; c.shg = d_shg.p;
@@ -1823,6 +1825,14 @@ int hier_create_impl(tpmg_context ctx, const tpmg_grid_desc* g, const tpmg_facto
           sw[c] = w2 * ge_e * ps[gw];
           ss[c] = w2 * ge_n * ps[gnc + gs];
         }
+      {  // one edge scalar on the whole global level (every rank takes the same decision, and
+         // the neighbours' ring columns of a decomposed run share it)
+        const double S0 = w2 * ge_e * ps[0];
+        bool uni = true;
+        for (int64_t G = 0; G < gnc && uni; ++G)
+          uni = (w2 * ge_e * ps[G] == S0) && (w2 * ge_n * ps[gnc + G] == S0);
+        L.uni = uni;
+      }
       L.d_bh.upload(L.bh.data(), L.plane);
       L.d_ah.upload(L.ah.data(), L.plane);
       L.d_xh.upload(L.xh.data(), L.plane);

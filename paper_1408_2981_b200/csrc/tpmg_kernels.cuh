@@ -28,7 +28,15 @@ struct VertCoef {      // HattedComponent::vert of beta, alpha_s, alpha_r, xi_r
 // Coefficient storage of a level (HattedComponent, discretization.hpp:32-48): factorised
 // (TPMG-tensor-product: vertical x horizontal factors), partial (alpha_r hat dense, the rest
 // factorised: MixedProfileSet, profiles.hpp:225-233), full (every component dense: ProfileSet).
-enum CoefMode { CM_FACT = 0, CM_PARTIAL = 1, CM_FULL = 2 };
+enum CoefMode { CM_FACT = 0, CM_PARTIAL = 1, CM_FULL = 2,
+                // kernel-side only (never a LevelCoef::cm): factorised coefficients whose four
+                // edge scalars coincide on the level (LevelCoef::uni): the edge product of a row
+                // is formed once instead of four times, same value
+                CM_UNI = 3 };
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+constexpr bool cm_fact(int cm) { return cm == CM_FACT || cm == CM_UNI; }
 
 struct LevelCoef {     // HattedComponent::horiz, per column of the local tile
   int nx, ny, nz;
@@ -41,6 +49,9 @@ struct LevelCoef {     // HattedComponent::horiz, per column of the local tile
   const double* ss;
   const double* sn;
   int cm = CM_FACT;
+  // factorised levels: sw == se == ss == sn in every column (isotropic horizontal coefficient on
+  // a square grid; then one value for the whole level, the edges being shared)
+  bool uni = false;
   // dense components, [k][y][x] like the fields (HattedComponent::dense):
   const double* ard = nullptr;  // alpha_r hat, nz+1 planes (partial, full)
   const double* bd = nullptr;   // beta hat, nz planes (full)
